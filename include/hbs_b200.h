@@ -1,0 +1,110 @@
+/*
+ * hbs_b200.h -- C-ABI of the B200-native HBS compress-from-samples path.
+ *
+ * Drop-in boundary for the hot path of the reference `hbs` package
+ * (arXiv 2205.02990, /root/reference/pkg/src/hbs):
+ *
+ *   reference (Python)                                   this ABI
+ *   ---------------------------------------------------  ------------------------------------
+ *   compress_from_samples, per-level body                 hbs_compress_level
+ *     (compress.py:250-269: compress_node_bases            (all boxes of one level, both sides)
+ *      155-175, compute_discrepancy 178-197,
+ *      lift_to_parent 200-227)
+ *   compress_from_samples, root (compress.py:271-279,     hbs_compress_root
+ *     compute_root 230-233)
+ *   nullspace / col / lstsq_right (linalg.py:35-90)       (inside the two calls above)
+ *   apply_matrix (factorization.py:89-143) = the HBS      hbs_apply
+ *     sampler behind hbs_oracle (operators.py:221-228)
+ *   dense_oracle a @ x / a.T @ x (operators.py:213-218)   hbs_dense_apply
+ *   IllConditionedProbeError(node_id, level)              per-box int32 status arrays
+ *     (errors.py:12-19, compress.py:260-265)                (+ HBS_ERR_ILL_CONDITIONED)
+ *
+ * Conventions.  All matrices are fp64, row-major (numpy C order).  Every
+ * pointer is a DEVICE pointer unless stated; the library allocates nothing:
+ * the caller passes a workspace sized by the *_workspace_bytes queries.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ * stream-ordered and never synchronise the host.
+ *
+ * Level geometry.  A level has `nbox` boxes; box b owns rows
+ * [row_begin[b], row_begin[b+1]) of the level's sample quadruple
+ * (leaf level: the global samples; coarser levels: the lifted 2r-row blocks).
+ * sq_off[b] = sum_{c<b} rows_c^2 (packed square blocks).
+ *
+ * Outputs of a level: U, V packed as (total_rows x r) with box b at row
+ * row_begin[b]; D packed as consecutive rows_b x rows_b blocks at sq_off[b];
+ * the lifted parent quadruple (nbox*r x s, child b at rows [b*r, (b+1)*r)).
+ */
+#ifndef HBS_B200_H_
+#define HBS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define HBS_OK 0
+#define HBS_ERR_DIMENSION 1        /* -> DimensionError */
+#define HBS_ERR_CONFIGURATION 2    /* -> ConfigurationError (nullity s - rows < r) */
+#define HBS_ERR_ILL_CONDITIONED 3  /* -> IllConditionedProbeError (see status) */
+#define HBS_ERR_CUDA 4
+#define HBS_ERR_WORKSPACE 5
+#define HBS_ERR_UNSUPPORTED 6
+
+/* Library version / build identification (sm_100a). */
+const char* hbs_b200_version(void);
+
+/* Workspace needed by hbs_compress_level for a level of `nbox` boxes of at
+ * most `max_rows` rows with s probes and rank r.  Replaces the reference's
+ * per-node temporaries (compress.py:155-227). */
+int hbs_level_workspace_bytes(int64_t nbox, int max_rows, int s, int r, size_t* bytes);
+
+/* One level of the sweep (compress.py:250-269 for every node of the level,
+ * plus lift_to_parent for the next level, compress.py:254-256/200-227).
+ *   omega, psi, y, z : level quadruple, rows x s, ld = s
+ *   u, v, d          : outputs (see header comment)
+ *   lift_*           : parent quadruple outputs (nbox*r x s) or all NULL
+ *   status           : int32[2*nbox]; status[side*nbox + b] != 0 marks box b's
+ *                      side (0: omega, 1: psi) as failing the sigma test of
+ *                      lstsq_right (linalg.py:73-78) with tolerance `tol`.
+ * Returns HBS_ERR_CONFIGURATION when s - max_rows < r (compress.py:164-168). */
+int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows,
+                       int s, int r, double tol,
+                       const double* omega, const double* psi, const double* y, const double* z,
+                       double* u, double* v, double* d,
+                       double* lift_omega, double* lift_psi, double* lift_y, double* lift_z,
+                       void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
+
+/* Root core D_root = Y_root Omega_root^+ (compress.py:230-233), rows = 2r.
+ * `row_begin`/`sq_off` describe the single root box ({0, 2r} / {0, 4r^2}). */
+int hbs_root_workspace_bytes(int rows, int s, size_t* bytes);
+int hbs_compress_root(const int64_t* row_begin, const int64_t* sq_off, int rows, int s, double tol,
+                      const double* omega, const double* y, double* root,
+                      void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
+
+/* Telescoping apply out = A q (transpose = 0) or A^T q (transpose = 1) of a
+ * packed factorization (factorization.py:89-143).  Host arrays of length
+ * depth+1 hold per-level DEVICE pointers (index 0 unused): row_begin[l],
+ * sq_off[l] (2^l + 1 entries each), u[l], v[l], d[l].  q, out: n x c. */
+int hbs_apply_workspace_bytes(int depth, int r, int64_t c, size_t* bytes);
+int hbs_apply(int depth, int r, int64_t n, int64_t c,
+              const int64_t* const* row_begin, const int64_t* const* sq_off,
+              const double* const* u, const double* const* v, const double* const* d,
+              const double* root, const double* q, double* out, int transpose,
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Dense sampler out = A q or A^T q for an explicit n x n row-major A
+ * (operators.py:213-218). */
+int hbs_dense_apply(int64_t n, int64_t c, const double* a, const double* q, double* out,
+                    int transpose, void* stream);
+
+/* Config-3 operator generator: A_ij = log|x_i - x_j| (i != j), A_ii = 1 with
+ * x_i = (cos t_i, 0.5 sin t_i), t_i = 2 pi i / n.  Fills rows [row0, row0+rows). */
+int hbs_fill_log_kernel(int64_t n, int64_t row0, int64_t rows, double* a, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBS_B200_H_ */

@@ -1,0 +1,296 @@
+"""Reference-compatible compression API on the B200 kernels.
+
+Mirrors `pkg/src/hbs/compress.py`: `CompressionConfig` (32-70), `SampleSet`
+(73-94), `draw_samples` (132-141), `compress_from_samples` (236-280) and
+`compress` (283-290).  The per-node Python loop of the reference is replaced
+by one C-ABI call per tree level (`hbs_compress_level`, all boxes of the
+level at once) plus `hbs_compress_root`; the sample quadruple, the lifted
+parent quadruples and the factorization stay resident in HBM.
+
+Error semantics follow the reference sweep order: the first failing node of
+the deepest failing level (ascending id) raises IllConditionedProbeError with
+its node id and level (compress.py:260-265, 274-279).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native, flops
+from .errors import ConfigurationError, DimensionError, IllConditionedProbeError
+from .factorization import HbsFactorization, tree_geometry
+from .tree import ClusterTree, build_tree
+
+DEFAULT_ILL_CONDITIONING_TOL = 1e-10   # linalg.py:20
+STREAM_OMEGA, STREAM_PSI, STREAM_POWER, STREAM_SYNTHETIC = 0, 1, 2, 3   # linalg.py:15-18
+
+
+@dataclass(frozen=True)
+class CompressionConfig:
+    """rank r, leaf threshold m, probe count s (None -> max(r + max leaf, 3r)),
+    seed, ill-conditioning tolerance (compress.py:32-70)."""
+
+    rank: int
+    leaf_threshold: int
+    probes: int | None = None
+    seed: int = 0
+    ill_conditioning_tol: float = DEFAULT_ILL_CONDITIONING_TOL
+
+    def resolved_probes(self, tree: ClusterTree) -> int:
+        if self.probes is not None:
+            return self.probes
+        return max(self.rank + tree.max_leaf_size, 3 * self.rank)
+
+    def validate_for(self, tree: ClusterTree) -> int:
+        if self.rank < 1:
+            raise ConfigurationError(f"rank must be positive, got {self.rank}")
+        if self.leaf_threshold < self.rank:
+            raise ConfigurationError(
+                f"leaf threshold {self.leaf_threshold} < rank {self.rank}: leaf bases would be wider than tall")
+        if tree.min_leaf_size < self.rank:
+            raise ConfigurationError(
+                f"smallest leaf has {tree.min_leaf_size} rows < rank {self.rank}; "
+                "lower the rank or raise the leaf threshold")
+        s = self.resolved_probes(tree)
+        s_min = max(self.rank + tree.max_leaf_size, 3 * self.rank)
+        if s < s_min:
+            raise ConfigurationError(f"probe count {s} below the required max(r + max leaf, 3r) = {s_min}")
+        return s
+
+
+@dataclass(frozen=True)
+class SampleSet:
+    """Probe quadruple (omega, psi, y = A omega, z = A^T psi): numpy arrays
+    (host) or float64 CUDA tensors (device-resident, no copy)."""
+
+    omega: object
+    psi: object
+    y: object
+    z: object
+
+    def __post_init__(self):
+        shapes = {tuple(m.shape) for m in (self.omega, self.psi, self.y, self.z)}
+        if len(shapes) != 1:
+            raise DimensionError(f"sample matrices must share one shape, got {shapes}")
+
+    @property
+    def n(self) -> int:
+        return self.omega.shape[0]
+
+    @property
+    def probes(self) -> int:
+        return self.omega.shape[1]
+
+
+def gaussian_matrix(n: int, s: int, seed: int, stream: int = 0) -> np.ndarray:
+    """Seeded n x s standard normals, the reference's PCG64 substreams
+    (linalg.py:23-32), so host samples are bit-identical to the reference's."""
+    if n < 1 or s < 1:
+        raise DimensionError(f"gaussian_matrix needs positive dimensions, got {n} x {s}")
+    gen = np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy=seed, spawn_key=(stream,))))
+    return gen.standard_normal((n, s))
+
+
+def draw_samples(oracle, s: int, seed: int) -> SampleSet:
+    """Draw Omega, Psi and push one batch through each oracle direction
+    (compress.py:132-141)."""
+    if s < 1:
+        raise DimensionError(f"need at least one probe column, got {s}")
+    omega = gaussian_matrix(oracle.n, s, seed, STREAM_OMEGA)
+    psi = gaussian_matrix(oracle.n, s, seed, STREAM_PSI)
+    return SampleSet(omega=omega, psi=psi, y=oracle.apply_batch(omega), z=oracle.apply_transpose_batch(psi))
+
+
+def _size_t():
+    return ctypes.c_size_t()
+
+
+class CompressPlan:
+    """Buffers + launch sequence of one (tree, s, r) compression on one device.
+
+    Everything is allocated up front, so `run()` only enqueues kernels on a
+    stream: it can be timed with CUDA events or captured in a CUDA graph."""
+
+    def __init__(self, tree: ClusterTree, s: int, rank: int, tol: float = DEFAULT_ILL_CONDITIONING_TOL,
+                 device=None, top_level: int = 1):
+        self.tree, self.s, self.rank, self.tol = tree, s, rank, tol
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.top_level = top_level   # levels L..top_level are compressed; top_level 1 => also the root
+        L, r = tree.depth, rank
+        self.geometry = tree_geometry(tree, r, self.device)
+        lib = _native.lib()
+        dev, f64 = self.device, torch.float64
+        self.levels = [None] * (L + 1)
+        ws = 0
+        for level in range(L, top_level - 1, -1):
+            g = self.geometry[level]
+            self.levels[level] = (torch.empty(g.total_rows, r, dtype=f64, device=dev),
+                                  torch.empty(g.total_rows, r, dtype=f64, device=dev),
+                                  torch.empty(g.sq_total, dtype=f64, device=dev))
+            sz = _size_t()
+            _native.check(lib.hbs_level_workspace_bytes(g.nbox, g.max_rows, s, r, ctypes.byref(sz)), "workspace")
+            ws = max(ws, sz.value)
+        sz = _size_t()
+        _native.check(lib.hbs_root_workspace_bytes(2 * r, s, ctypes.byref(sz)), "workspace")
+        ws = max(ws, sz.value)
+        self.workspace = torch.empty(ws // 8 + 1, dtype=f64, device=dev)
+        self.workspace_bytes = ws
+        # lifted quadruples, ping-pong: level l writes 2^l * r rows
+        big = (1 << L) * r
+        self.lift = [[torch.empty(rows, s, dtype=f64, device=dev) for _ in range(4)]
+                     for rows in (big, max(big // 2, 2 * r))]
+        nstat = sum(2 * (1 << lv) for lv in range(top_level, L + 1)) + 1
+        self.status = torch.zeros(nstat, dtype=torch.int32, device=dev)
+        self.root = torch.empty(2 * r, 2 * r, dtype=f64, device=dev)
+        self.top_quad = None   # lifted quadruple feeding level top_level - 1 (multi-GPU hand-off)
+
+    def _status_slices(self):
+        out, off = {}, 0
+        for level in range(self.tree.depth, self.top_level - 1, -1):
+            n = 2 * (1 << level)
+            out[level] = self.status[off:off + n]
+            off += n
+        out[0] = self.status[off:off + 1]
+        return out
+
+    def run(self, omega, psi, y, z, stream=None):
+        """Enqueue the level sweep (compress.py:250-279) on `stream`."""
+        lib = _native.lib()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        L, r, s = self.tree.depth, self.rank, self.s
+        stat = self._status_slices()
+        quad = (omega, psi, y, z)
+        for idx, level in enumerate(range(L, self.top_level - 1, -1)):
+            g = self.geometry[level]
+            u, v, d = self.levels[level]
+            out = self.lift[idx % 2]
+            rc = lib.hbs_compress_level(
+                g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.max_rows, s, r, self.tol,
+                quad[0].data_ptr(), quad[1].data_ptr(), quad[2].data_ptr(), quad[3].data_ptr(),
+                u.data_ptr(), v.data_ptr(), d.data_ptr(),
+                out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), out[3].data_ptr(),
+                self.workspace.data_ptr(), self.workspace_bytes, stat[level].data_ptr(), st)
+            _native.check(rc, f"hbs_compress_level(level {level})")
+            rows = g.nbox * r
+            quad = tuple(m[:rows] for m in out)
+        self.top_quad = quad
+        if self.top_level == 1:
+            g0 = self.geometry[0]
+            rc = lib.hbs_compress_root(g0.row_begin.data_ptr(), g0.sq_off.data_ptr(), 2 * r, s, self.tol,
+                                       quad[0].data_ptr(), quad[2].data_ptr(), self.root.data_ptr(),
+                                       self.workspace.data_ptr(), self.workspace_bytes, stat[0].data_ptr(), st)
+            _native.check(rc, "hbs_compress_root")
+
+    def raise_for_status(self):
+        """One device->host read of all per-box statuses; raise like the
+        reference for the first failing node in sweep order."""
+        host = self.status.cpu().numpy()
+        if not host.any():
+            return
+        off = 0
+        for level in range(self.tree.depth, self.top_level - 1, -1):
+            nbox = 1 << level
+            blk = host[off:off + 2 * nbox].reshape(2, nbox)
+            off += 2 * nbox
+            bad = np.nonzero(blk.any(axis=0))[0]
+            if bad.size:
+                j = int(bad[0])
+                nid = (1 << level) - 1 + j
+                raise IllConditionedProbeError(
+                    f"node {nid} (level {level}): probe matrix is rank deficient within tolerance "
+                    f"{self.tol:g}; increase the probe count s", node_id=nid, level=level)
+        if self.top_level == 1 and host[off]:
+            raise IllConditionedProbeError(
+                f"node 0 (level 0): probe matrix is rank deficient within tolerance {self.tol:g}; "
+                "increase the probe count s", node_id=0, level=0)
+
+    def factorization(self) -> HbsFactorization:
+        return HbsFactorization.from_device(self.tree, self.rank, self.geometry, self.levels, self.root)
+
+
+def _check_configuration(tree: ClusterTree, s: int, r: int):
+    """Shape-only failures of compress_node_bases / col, in sweep order
+    (compress.py:164-168, linalg.py:329-331)."""
+    for level in range(tree.depth, 0, -1):
+        sizes = tree.level_sizes(level) if level == tree.depth else np.full(1 << level, 2 * r)
+        short = np.nonzero(s - sizes < r)[0]
+        thin = np.nonzero(sizes < r)[0]
+        if short.size or thin.size:
+            first = min(short.min() if short.size else 1 << 62, thin.min() if thin.size else 1 << 62)
+            rows = int(sizes[first])
+            if s - rows < r:
+                raise ConfigurationError(
+                    f"probe count {s} leaves nullity {s - rows} < rank {r} for a {rows}-row node; "
+                    "increase the probe count s")
+            raise DimensionError(f"cannot extract {r} basis columns from a {rows} x {r} matrix")
+
+
+def _device_tensor(a, device):
+    if isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64:
+            raise DimensionError(f"samples must be float64, got {a.dtype}")
+        return a.to(device).contiguous()
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    t = torch.from_numpy(arr)
+    if device.type == "cuda":
+        t = t.pin_memory().to(device, non_blocking=True)
+    return t
+
+
+def _charge_madds(tree: ClusterTree, s: int, r: int):
+    """Host-side madd charge identical to the reference's per-node calls."""
+    total = 0
+    for level in range(tree.depth, 0, -1):
+        sizes = tree.level_sizes(level) if level == tree.depth else np.full(1 << level, 2 * r)
+        for rows in np.unique(sizes):
+            cnt = int((sizes == rows).sum())
+            total += cnt * (flops.node_compress_madds(int(rows), s, r) + flops.lift_madds(int(rows), s, r))
+    total += flops.root_madds(2 * r, s)
+    flops.add_madds(total)
+
+
+_PLANS = {}
+
+
+def get_plan(tree: ClusterTree, s: int, r: int, tol: float, device) -> CompressPlan:
+    key = (tree.n, tree.leaf_threshold, s, r, tol, str(device))
+    plan = _PLANS.get(key)
+    if plan is None:
+        _PLANS.clear()          # keep at most one plan's buffers alive
+        plan = _PLANS[key] = CompressPlan(tree, s, r, tol, device)
+    return plan
+
+
+def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: CompressionConfig,
+                          device=None) -> HbsFactorization:
+    """Level sweep on an already-drawn probe quadruple (compress.py:236-280),
+    on the GPU.  Host (numpy) samples are uploaded once; CUDA tensors are used
+    in place.  The returned factorization is device-resident."""
+    if samples.n != tree.n:
+        raise DimensionError(f"samples are for n={samples.n}, tree has n={tree.n}")
+    s, r = samples.probes, config.rank
+    _check_configuration(tree, s, r)
+    if device is None:
+        dev = samples.omega.device if isinstance(samples.omega, torch.Tensor) else torch.device("cuda")
+    else:
+        dev = torch.device(device)
+    if dev.type != "cuda":
+        raise DimensionError("the compressor runs on a CUDA device only (no CPU fallback)")
+    quad = [_device_tensor(m, dev) for m in (samples.omega, samples.psi, samples.y, samples.z)]
+    plan = CompressPlan(tree, s, r, config.ill_conditioning_tol, dev)
+    plan.run(*quad)
+    plan.raise_for_status()
+    if flops.counting():
+        _charge_madds(tree, s, r)
+    return plan.factorization()
+
+
+def compress(oracle, config: CompressionConfig) -> HbsFactorization:
+    """Build the tree, draw exactly s probes per direction, sweep
+    (compress.py:283-290)."""
+    tree = build_tree(oracle.n, config.leaf_threshold)
+    s = config.validate_for(tree)
+    samples = draw_samples(oracle, s, config.seed)
+    return compress_from_samples(samples, tree, config)

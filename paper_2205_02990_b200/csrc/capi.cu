@@ -1,0 +1,337 @@
+// C-ABI implementation (include/hbs_b200.h): level orchestration of the
+// batched kernels, workspace carving, and the samplers.
+#include <cmath>
+#include <cstring>
+#include "../../include/hbs_b200.h"
+#include "kernels.h"
+
+namespace hbs {
+namespace {
+
+constexpr size_t kAlign = 256;
+
+struct Carver {
+  char* base;
+  size_t used = 0;
+  template <typename T>
+  T* take(size_t count) {
+    used = (used + kAlign - 1) / kAlign * kAlign;
+    T* p = base ? reinterpret_cast<T*>(base + used) : nullptr;
+    used += count * sizeof(T);
+    return p;
+  }
+};
+
+// Per-level scratch (uniform per-box strides, max_rows = nr).
+struct LevelWs {
+  double* vt[2]; double* R[2]; double* tau[2]; double* T[2]; double* Rinv[2];
+  double* X[2];   // Y Omega^+ and Z Psi^+
+  double* P[2];   // Y P and Z Q
+  double* G1; double* M3; double* M4; double* E1; double* E2;
+  double* gscratch;
+};
+
+size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bool root_only) {
+  const size_t nb = (size_t)nbox;
+  const int npanel = (nr + kNB - 1) / kNB;
+  const int sides = root_only ? 1 : 2;
+  for (int sd = 0; sd < 2; ++sd) {
+    const bool on = sd < sides;
+    w.vt[sd] = on ? c.take<double>(nb * nr * s) : nullptr;
+    w.R[sd] = on ? c.take<double>(nb * nr * nr) : nullptr;
+    w.tau[sd] = on ? c.take<double>(nb * nr) : nullptr;
+    w.T[sd] = on ? c.take<double>(nb * npanel * kNB * kNB) : nullptr;
+    w.Rinv[sd] = on ? c.take<double>(nb * npanel * kNB * kNB) : nullptr;
+    w.X[sd] = on ? c.take<double>(nb * nr * nr) : nullptr;
+    w.P[sd] = (on && !root_only) ? c.take<double>(nb * nr * r) : nullptr;
+  }
+  if (!root_only) {
+    w.G1 = c.take<double>(nb * r * nr);
+    w.M3 = c.take<double>(nb * r * r);
+    w.M4 = c.take<double>(nb * r * nr);
+    w.E1 = c.take<double>(nb * r * nr);
+    w.E2 = c.take<double>(nb * r * nr);
+  } else {
+    w.G1 = w.M3 = w.M4 = w.E1 = w.E2 = nullptr;
+  }
+  const bool big_factor = geqrf_smem_bytes(s, nr, kGeqrfFactor) > kMaxSmemBytes;
+  const bool big_ortho = geqrf_smem_bytes(nr, r, kGeqrfOrtho) > kMaxSmemBytes;
+  w.gscratch = (big_factor || big_ortho)
+                   ? c.take<double>(geqrf_scratch_doubles(s > nr ? s : nr, nr > r ? nr : r, nbox))
+                   : nullptr;
+  return c.used + kAlign;
+}
+
+BOperand op(const double* p, int64_t c_rb, int64_t c_b, int64_t c_sq, int ld, bool ld_rows, bool trans) {
+  BOperand o;
+  o.p = p; o.c_rb = c_rb; o.c_b = c_b; o.c_sq = c_sq;
+  o.ld_fixed = ld; o.ld_rows = ld_rows ? 1 : 0; o.trans = trans ? 1 : 0;
+  return o;
+}
+BDim dfix(int v) { return BDim{v, 0}; }
+BDim drows() { return BDim{0, 1}; }
+
+int gemm(const LevelGeo& geo, BDim M, BDim N, BDim K, int mmax, int nmax, BOperand A, BOperand B,
+         double* C, int64_t cc_rb, int64_t cc_b, int64_t cc_sq, int ldc, bool ldc_rows, double alpha,
+         double beta, BOperand C0, cudaStream_t st) {
+  BgemmArgs a;
+  a.geo = geo; a.M = M; a.N = N; a.K = K; a.M_max = mmax; a.N_max = nmax;
+  a.A = A; a.B = B; a.C0 = C0;
+  a.C = C; a.cc_rb = cc_rb; a.cc_b = cc_b; a.cc_sq = cc_sq; a.ldc_fixed = ldc; a.ldc_rows = ldc_rows ? 1 : 0;
+  a.alpha = alpha; a.beta = beta;
+  return launch_bgemm(a, st);
+}
+
+#define HBS_TRY(x) do { int _e = (x); if (_e != kOk) return _e; } while (0)
+
+// Probe factorisation + apply/solve for both sides of a level (or side 0 only).
+int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int nsides,
+                     const double* om0, const double* om1, const double* y0, const double* y1,
+                     LevelWs& w, int32_t* status, double* root_out, cudaStream_t st) {
+  GeqrfArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = geo; g.mode = kGeqrfFactor;
+  g.m_fixed = s; g.m_is_rows = 0; g.n_fixed = 0; g.n_is_rows = 1;
+  g.m_max = s; g.n_max = nr; g.tol = tol; g.gscratch = w.gscratch;
+  const double* oms[2] = {om0, om1};
+  for (int sd = 0; sd < nsides; ++sd) {
+    GeqrfSide& S = g.side[sd];
+    S.src = oms[sd]; S.src_c_rb = s; S.src_c_b = 0; S.src_rs = 1; S.src_cs = s;
+    S.vt = w.vt[sd]; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
+    S.r = w.R[sd]; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
+    S.tau = w.tau[sd]; S.tau_stride = nr;
+    S.status = status + sd * geo.nbox;
+  }
+  HBS_TRY(launch_geqrf(g, nsides, st));
+
+  const int npanel = (nr + kNB - 1) / kNB;
+  PanelArgs p;
+  std::memset(&p, 0, sizeof(p));
+  p.geo = geo; p.m = s; p.n_fixed = 0; p.n_is_rows = 1; p.n_max = nr;
+  for (int sd = 0; sd < nsides; ++sd) {
+    PanelSide& S = p.side[sd];
+    S.vt = w.vt[sd]; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
+    S.r = w.R[sd]; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
+    S.tau = w.tau[sd]; S.tau_stride = nr;
+    S.t = w.T[sd]; S.t_stride = (int64_t)npanel * kNB * kNB;
+    S.rinv = w.Rinv[sd]; S.rinv_stride = (int64_t)npanel * kNB * kNB;
+  }
+  HBS_TRY(launch_panel_factors(p, nsides, st));
+
+  ApplyQArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.geo = geo; a.s = s; a.r = r; a.n_fixed = 0; a.n_is_rows = 1; a.n_max = nr;
+  const double* ys[2] = {y0, y1};
+  for (int sd = 0; sd < nsides; ++sd) {
+    ApplyQSide& S = a.side[sd];
+    S.y = ys[sd]; S.y_c_rb = s; S.y_c_b = 0; S.ldy = s;
+    S.vt = w.vt[sd]; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
+    S.r = w.R[sd]; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
+    S.t = w.T[sd]; S.t_stride = (int64_t)npanel * kNB * kNB;
+    S.rinv = w.Rinv[sd]; S.rinv_stride = (int64_t)npanel * kNB * kNB;
+    if (root_out) {
+      S.x = root_out; S.x_stride = 0; S.ldx = nr;
+      S.yp = nullptr;
+    } else {
+      S.x = w.X[sd]; S.x_stride = (int64_t)nr * nr; S.ldx = nr;
+      S.yp = w.P[sd]; S.yp_stride = (int64_t)nr * r; S.ldyp = r;
+    }
+  }
+  return launch_applyq(a, nsides, st);
+}
+
+}  // namespace
+}  // namespace hbs
+
+using namespace hbs;
+
+extern "C" {
+
+const char* hbs_b200_version(void) { return "hbs_b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int hbs_level_workspace_bytes(int64_t nbox, int max_rows, int s, int r, size_t* bytes) {
+  if (nbox < 1 || max_rows < 1 || s < 1 || r < 1 || !bytes) return HBS_ERR_DIMENSION;
+  Carver c{nullptr};
+  LevelWs w;
+  *bytes = carve_level(c, w, nbox, max_rows, s, r, false);
+  return HBS_OK;
+}
+
+int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int s,
+                       int r, double tol, const double* omega, const double* psi, const double* y,
+                       const double* z, double* u, double* v, double* d, double* lift_omega,
+                       double* lift_psi, double* lift_y, double* lift_z, void* workspace,
+                       size_t workspace_bytes, int32_t* status, void* stream) {
+  if (nbox < 1 || max_rows < 1 || s < 1 || r < 1 || max_rows < r) return HBS_ERR_DIMENSION;
+  if (s - max_rows < r) return HBS_ERR_CONFIGURATION;
+  if (s > 512) return HBS_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver c{static_cast<char*>(workspace)};
+  LevelWs w;
+  if (carve_level(c, w, nbox, max_rows, s, r, false) > workspace_bytes) return HBS_ERR_WORKSPACE;
+  const LevelGeo geo{row_begin, sq_off, nbox};
+  const int nr = max_rows;
+
+  HBS_TRY(factor_and_solve(geo, nr, s, r, tol, 2, omega, psi, y, z, w, status, nullptr, st));
+
+  // U = col(Y P), V = col(Z Q): Householder QR + explicit Q (linalg.py:35-49).
+  GeqrfArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = geo; g.mode = kGeqrfOrtho;
+  g.m_fixed = 0; g.m_is_rows = 1; g.n_fixed = r; g.n_is_rows = 0;
+  g.m_max = nr; g.n_max = r; g.tol = tol; g.gscratch = w.gscratch;
+  double* outs[2] = {u, v};
+  for (int sd = 0; sd < 2; ++sd) {
+    GeqrfSide& S = g.side[sd];
+    S.src = w.P[sd]; S.src_c_rb = 0; S.src_c_b = (int64_t)nr * r; S.src_rs = r; S.src_cs = 1;
+    S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
+  }
+  HBS_TRY(launch_geqrf(g, 2, st));
+
+  // Discrepancy D = X - U [U^T X - U^T W^T + (U^T W^T V) V^T]  (compress.py:192-197)
+  const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
+  const BOperand Ut = op(u, r, 0, 0, r, false, true);   // U^T  (r x rows)
+  const BOperand Un = op(u, r, 0, 0, r, false, false);  // U    (rows x r)
+  const BOperand Vt = op(v, r, 0, 0, r, false, true);
+  const BOperand Vn = op(v, r, 0, 0, r, false, false);
+  const int64_t sqs = (int64_t)nr * nr, rs = (int64_t)r * nr;
+  const BOperand Xn = op(w.X[0], 0, sqs, 0, nr, false, false);
+  const BOperand Wt = op(w.X[1], 0, sqs, 0, nr, false, true);
+  const BOperand G1 = op(w.G1, 0, rs, 0, nr, false, false);
+  const BOperand M3 = op(w.M3, 0, (int64_t)r * r, 0, r, false, false);
+  const BOperand M4 = op(w.M4, 0, rs, 0, nr, false, false);
+  HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Wt, w.G1, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
+  HBS_TRY(gemm(geo, dfix(r), dfix(r), drows(), r, r, G1, Vn, w.M3, 0, (int64_t)r * r, 0, r, false, 1.0, 0.0,
+               none, st));
+  HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Xn, w.M4, 0, rs, 0, nr, false, 1.0, -1.0, G1, st));
+  HBS_TRY(gemm(geo, dfix(r), drows(), dfix(r), r, nr, M3, Vt, w.M4, 0, rs, 0, nr, false, 1.0, 1.0, M4, st));
+  HBS_TRY(gemm(geo, drows(), drows(), dfix(r), nr, nr, Un, M4, d, 0, 0, 1, 0, true, -1.0, 1.0, Xn, st));
+
+  if (lift_omega) {
+    // Parent quadruple rows of child b: [b*r, (b+1)*r)  (compress.py:209-227)
+    const BOperand Dn = op(d, 0, 0, 1, 0, true, false);
+    const BOperand Dt = op(d, 0, 0, 1, 0, true, true);
+    const BOperand E1 = op(w.E1, 0, rs, 0, nr, false, false);
+    const BOperand E2 = op(w.E2, 0, rs, 0, nr, false, false);
+    HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Dn, w.E1, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Vt, Dt, w.E2, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
+    const BOperand Om = op(omega, s, 0, 0, s, false, false);
+    const BOperand Ps = op(psi, s, 0, 0, s, false, false);
+    const BOperand Yn = op(y, s, 0, 0, s, false, false);
+    const BOperand Zn = op(z, s, 0, 0, s, false, false);
+    const int64_t prs = (int64_t)r * s;
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Om, lift_omega, 0, prs, 0, s, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Ps, lift_psi, 0, prs, 0, s, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Yn, lift_y, 0, prs, 0, s, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E1, Om, lift_y, 0, prs, 0, s, false, -1.0, 1.0,
+                 op(lift_y, 0, prs, 0, s, false, false), st));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Zn, lift_z, 0, prs, 0, s, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E2, Ps, lift_z, 0, prs, 0, s, false, -1.0, 1.0,
+                 op(lift_z, 0, prs, 0, s, false, false), st));
+  }
+  return HBS_OK;
+}
+
+int hbs_root_workspace_bytes(int rows, int s, size_t* bytes) {
+  if (rows < 1 || s < 1 || !bytes) return HBS_ERR_DIMENSION;
+  Carver c{nullptr};
+  LevelWs w;
+  *bytes = carve_level(c, w, 1, rows, s, 1, true);
+  return HBS_OK;
+}
+
+int hbs_compress_root(const int64_t* row_begin, const int64_t* sq_off, int rows, int s, double tol,
+                      const double* omega, const double* y, double* root, void* workspace,
+                      size_t workspace_bytes, int32_t* status, void* stream) {
+  if (rows < 1 || s < rows) return HBS_ERR_DIMENSION;
+  if (s > 512) return HBS_ERR_UNSUPPORTED;
+  Carver c{static_cast<char*>(workspace)};
+  LevelWs w;
+  if (carve_level(c, w, 1, rows, s, 1, true) > workspace_bytes) return HBS_ERR_WORKSPACE;
+  const LevelGeo geo{row_begin, sq_off, 1};
+  return factor_and_solve(geo, rows, s, 1, tol, 1, omega, nullptr, y, nullptr, w, status, root,
+                          static_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------------------------ samplers
+int hbs_apply_workspace_bytes(int depth, int r, int64_t c, size_t* bytes) {
+  if (depth < 1 || r < 1 || c < 1 || !bytes) return HBS_ERR_DIMENSION;
+  // qhat and uhat for every level: sum_l 2^l r c, twice.
+  const size_t per = ((size_t(1) << (depth + 1)) - 2) * (size_t)r * (size_t)c;
+  *bytes = 2 * per * sizeof(double) + 2 * kAlign;
+  return HBS_OK;
+}
+
+int hbs_apply(int depth, int r, int64_t n, int64_t c, const int64_t* const* row_begin,
+              const int64_t* const* sq_off, const double* const* u, const double* const* v,
+              const double* const* d, const double* root, const double* q, double* out, int transpose,
+              void* workspace, size_t workspace_bytes, void* stream) {
+  if (depth < 1 || r < 1 || n < 2 || c < 1) return HBS_ERR_DIMENSION;
+  if (c > (1 << 30)) return HBS_ERR_UNSUPPORTED;
+  size_t need;
+  hbs_apply_workspace_bytes(depth, r, c, &need);
+  if (need > workspace_bytes) return HBS_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cc = (int)c;
+  // level buffers: qhat[l], uhat[l] hold 2^l * r rows of c columns
+  double* base = static_cast<double*>(workspace);
+  double* qhat[64];
+  double* uhat[64];
+  size_t off = 0;
+  for (int l = 1; l <= depth; ++l) { qhat[l] = base + off; off += ((size_t)1 << l) * r * c; }
+  for (int l = 1; l <= depth; ++l) { uhat[l] = base + off; off += ((size_t)1 << l) * r * c; }
+  const double* const* up = transpose ? u : v;
+  const double* const* down = transpose ? v : u;
+  const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
+  // leaf rows: max rows of the leaf level
+  const int leaf_max = (int)((n + ((int64_t)1 << depth) - 1) >> depth);
+  // upward pass (factorization.py:111-119)
+  for (int l = depth; l >= 1; --l) {
+    const LevelGeo geo{row_begin[l], sq_off[l], (int64_t)1 << l};
+    const double* src = (l == depth) ? q : qhat[l + 1];
+    HBS_TRY(gemm(geo, dfix(r), dfix(cc), drows(), r, cc, op(up[l], r, 0, 0, r, false, true),
+                 op(src, cc, 0, 0, cc, false, false), qhat[l], 0, (int64_t)r * cc, 0, cc, false, 1.0, 0.0,
+                 none, st));
+  }
+  // root (factorization.py:121-125): uhat[1] = D_root^(T) qhat[1]
+  {
+    const LevelGeo geo{nullptr, nullptr, 1};
+    HBS_TRY(gemm(geo, dfix(2 * r), dfix(cc), dfix(2 * r), 2 * r, cc, op(root, 0, 0, 0, 2 * r, false, transpose != 0),
+                 op(qhat[1], 0, 0, 0, cc, false, false), uhat[1], 0, 0, 0, cc, false, 1.0, 0.0, none, st));
+  }
+  // downward pass (factorization.py:127-142)
+  for (int l = 1; l <= depth; ++l) {
+    const LevelGeo geo{row_begin[l], sq_off[l], (int64_t)1 << l};
+    const bool leaf = (l == depth);
+    double* dst = leaf ? out : uhat[l + 1];
+    const double* rhs = leaf ? q : qhat[l + 1];
+    const int mmax = leaf ? leaf_max : 2 * r;
+    HBS_TRY(gemm(geo, drows(), dfix(cc), dfix(r), mmax, cc, op(down[l], r, 0, 0, r, false, false),
+                 op(uhat[l], 0, (int64_t)r * cc, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 0.0,
+                 none, st));
+    HBS_TRY(gemm(geo, drows(), dfix(cc), drows(), mmax, cc, op(d[l], 0, 0, 1, 0, true, transpose != 0),
+                 op(rhs, cc, 0, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 1.0,
+                 op(dst, cc, 0, 0, cc, false, false), st));
+  }
+  return HBS_OK;
+}
+
+int hbs_dense_apply(int64_t n, int64_t c, const double* a, const double* q, double* out, int transpose,
+                    void* stream) {
+  if (n < 1 || c < 1) return HBS_ERR_DIMENSION;
+  if (n > (1 << 30) || c > (1 << 30)) return HBS_ERR_UNSUPPORTED;
+  // single "box" spanning all rows: geometry {0, n}
+  static_assert(sizeof(int64_t) == 8, "");
+  const int nn = (int)n, cc = (int)c;
+  BgemmArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = LevelGeo{nullptr, nullptr, 1};
+  g.M = dfix(nn); g.N = dfix(cc); g.K = dfix(nn); g.M_max = nn; g.N_max = cc;
+  g.A = op(a, 0, 0, 0, nn, false, transpose != 0);
+  g.B = op(q, 0, 0, 0, cc, false, false);
+  g.C0 = op(nullptr, 0, 0, 0, 0, false, false);
+  g.C = out; g.ldc_fixed = cc; g.alpha = 1.0; g.beta = 0.0;
+  return launch_bgemm(g, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

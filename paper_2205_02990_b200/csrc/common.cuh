@@ -1,0 +1,67 @@
+// Shared device helpers for the HBS compress-from-samples kernels (sm_100a, fp64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define HBS_DEV __device__ __forceinline__
+
+namespace hbs {
+
+// Per-box status written by the kernels (0 = ok).  The host maps a nonzero
+// status onto IllConditionedProbeError(node_id, level) -- errors.py:12-19.
+enum BoxStatus : int32_t { kBoxOk = 0, kBoxIllConditioned = 1 };
+
+// Panel width of the blocked Householder representation (compact WY T blocks,
+// diagonal-block inverses of R).
+constexpr int kNB = 32;
+
+// Row geometry of one tree level: box b owns rows [row_begin[b], row_begin[b+1]).
+struct LevelGeo {
+  const int64_t* row_begin;  // nbox + 1
+  const int64_t* sq_off;     // nbox + 1, prefix sums of rows^2 (packed D blocks)
+  int64_t nbox;
+};
+
+HBS_DEV int box_rows(const LevelGeo& g, int64_t b) {
+  return static_cast<int>(g.row_begin[b + 1] - g.row_begin[b]);
+}
+
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
+// Fragment ownership (lane = 4*g + t): A(g, t); B(t, g); C(g, 2t), C(g, 2t+1).
+HBS_DEV void dmma8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+HBS_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+HBS_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+HBS_DEV double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Leading dimension (in doubles) for an smem tile whose rows hold `cols`
+// doubles: rounded up so ld % 16 == 4, which makes every m8n8k4 fragment load
+// (row- or column-ordered) bank-conflict free.
+
+inline __host__ __device__ int frag_ld(int cols) {
+  int ld = (cols + 3) & ~3;
+  while ((ld & 15) != 4) ld += 4;
+  return ld;
+}
+
+inline __host__ __device__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace hbs

@@ -1,0 +1,115 @@
+// Internal (C++) launch interface of the HBS kernels.  The public C-ABI lives
+// in include/hbs_b200.h and is implemented in capi.cu on top of these.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace hbs {
+
+enum Status : int {
+  kOk = 0,
+  kErrDimension = 1,      // -> DimensionError
+  kErrConfiguration = 2,  // -> ConfigurationError
+  kErrIllConditioned = 3, // -> IllConditionedProbeError (see status arrays)
+  kErrCuda = 4,
+  kErrWorkspace = 5,
+  kErrUnsupported = 6,
+};
+
+constexpr size_t kMaxSmemBytes = 227 * 1024;
+
+// ---------------------------------------------------------------- geqrf
+enum GeqrfMode : int { kGeqrfFactor = 0, kGeqrfOrtho = 1 };
+
+struct GeqrfSide {
+  // source: element (i, j) of box b at src + src_c_rb*row_begin[b] + src_c_b*b + i*src_rs + j*src_cs
+  const double* src;
+  int64_t src_c_rb, src_c_b;
+  int64_t src_rs, src_cs;
+  // kFactor outputs (uniform per-box strides)
+  double* vt; int64_t vt_stride; int ldvt;
+  double* r; int64_t r_stride; int ldr;
+  double* tau; int64_t tau_stride;
+  int32_t* status;
+  // kOrtho output: q + q_c_rb*row_begin[b] + q_c_b*b, row-major, ld = ldq
+  double* q; int64_t q_c_rb, q_c_b; int ldq;
+};
+
+struct GeqrfArgs {
+  LevelGeo geo;
+  GeqrfSide side[2];
+  int mode;
+  int m_fixed, n_fixed, m_is_rows, n_is_rows;
+  int m_max, n_max, lda_max;
+  double tol;
+  double* gscratch;  // needed when the matrix does not fit in shared memory
+  int use_smem;
+};
+
+size_t geqrf_smem_bytes(int m_max, int n_max, int mode);
+size_t geqrf_scratch_doubles(int m_max, int n_max, int64_t nbox);
+int launch_geqrf(GeqrfArgs args, int nsides, cudaStream_t stream);
+
+// ---------------------------------------------------------------- panel factors
+// Per (box, side, panel): compact-WY T block (dlarft, forward/columnwise) of
+// the reflectors j0..j0+NB-1 and the inverse of R's diagonal block.
+struct PanelSide {
+  const double* vt; int64_t vt_stride; int ldvt;
+  const double* r; int64_t r_stride; int ldr;
+  const double* tau; int64_t tau_stride;
+  double* t; int64_t t_stride;        // npanel * NB * NB per box, row-major NB x NB blocks
+  double* rinv; int64_t rinv_stride;  // same shape
+};
+struct PanelArgs {
+  LevelGeo geo;
+  PanelSide side[2];
+  int m;       // reflector length (s)
+  int n_fixed, n_is_rows, n_max;
+};
+int launch_panel_factors(PanelArgs args, int nsides, cudaStream_t stream);
+
+// ---------------------------------------------------------------- apply Q + solve
+// Per (row tile, box, side): Yt <- Y_tile * Q (blocked WY), then
+// X_tile = (Y Q)(:, 0:n) R^{-T} and P-projection = (Y Q)(:, s-r:s).
+struct ApplyQSide {
+  const double* y; int64_t y_c_rb, y_c_b; int ldy;  // rows of Y for box b (row-major, ld)
+  const double* vt; int64_t vt_stride; int ldvt;
+  const double* r; int64_t r_stride; int ldr;
+  const double* t; int64_t t_stride;
+  const double* rinv; int64_t rinv_stride;
+  double* x; int64_t x_stride; int ldx;      // n_b x n_b per box (uniform stride)
+  double* yp; int64_t yp_stride; int ldyp;   // n_b x r per box (may be null)
+};
+struct ApplyQArgs {
+  LevelGeo geo;
+  ApplyQSide side[2];
+  int s, r;
+  int n_fixed, n_is_rows, n_max;
+};
+int launch_applyq(ApplyQArgs args, int nsides, cudaStream_t stream);
+
+// ---------------------------------------------------------------- batched GEMM
+// Operand addressing for box b: base + c_rb*row_begin[b] + c_b*b + c_sq*sq_off[b];
+// element (i, j) at [i*ld + j] (trans = 0) or [j*ld + i] (trans = 1);
+// ld = ld_fixed, or the box's row count when ld_rows != 0.
+struct BOperand {
+  const double* p;
+  int64_t c_rb, c_b, c_sq;
+  int ld_fixed, ld_rows, trans;
+};
+struct BDim {
+  int fixed, rows_mult;  // value = fixed + rows_mult * rows_b
+};
+struct BgemmArgs {
+  LevelGeo geo;
+  BDim M, N, K;
+  int M_max, N_max;
+  BOperand A, B, C0;
+  double* C; int64_t cc_rb, cc_b, cc_sq; int ldc_fixed, ldc_rows;
+  double alpha, beta;  // C = alpha * op(A) op(B) + beta * C0
+};
+int launch_bgemm(const BgemmArgs& args, cudaStream_t stream);
+
+}  // namespace hbs

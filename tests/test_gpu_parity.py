@@ -1,0 +1,140 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference's golden fixtures.
+
+Parity contract:
+  * oversampled twins (r > k): ||(A_gpu - A_ref) x|| / ||A_ref x|| <= 1e-10;
+  * literal configs (r = k, rounding-chaotic in the reference itself):
+    ||(A_gpu - A) x|| / ||A x|| <= 10 x the reference's own error vs the truth;
+  * node-level: projectors U U^T, V V^T and D of the first leaf / level-1 node
+    within 1e-10 of the reference when the case is well conditioned.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2205_02990_b200 as hb
+from oracle import hbs_oracle as O
+from tests import golden_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_cases.names()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    hb._native.lib()   # fail loudly if the extension is missing
+
+
+def gpu_compress(samples, n, leaf, r, tol=1e-10):
+    tree = hb.build_tree(n, leaf)
+    return hb.compress_from_samples(hb.SampleSet(*samples), tree,
+                                    hb.CompressionConfig(rank=r, leaf_threshold=leaf, ill_conditioning_tol=tol))
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_operator_parity(name):
+    c = golden_cases.load(name)
+    g = c["fixture"]
+    f = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    ax = hb.apply_matrix(f, c["x"])
+    atx = hb.apply_matrix(f, c["x"], transpose=True)
+    ref_err = float(g["ref_err_vs_truth"])
+    err_truth = rel(ax, g["true_ax"])
+    if c["literal"]:
+        assert err_truth <= 10.0 * ref_err, (err_truth, ref_err)
+    else:
+        assert rel(ax, g["ref_ax"]) <= 1e-10
+        assert rel(atx, g["ref_atx"]) <= 1e-10
+        assert err_truth <= 1e-10
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "literal" in n and "c3" not in n])
+def test_leaf_projectors_literal(name):
+    """r == k and nullity == r at the leaves: span(U), span(V) and D of a leaf
+    are unique, so they must match the reference's node for node.  (Config 3
+    is excluded: its leaf samples Y P are numerically rank deficient --
+    sigma_min/sigma_max ~ 3e-17 -- so span(U) is rounding-determined there,
+    in the reference as much as here.)"""
+    c = golden_cases.load(name)
+    g = c["fixture"]
+    f = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    nid = int(g["leaf_id"])
+    u, v, d = f.u_bases[nid], f.v_bases[nid], f.discs[nid]
+    ur, vr, dr = g["leaf_u"], g["leaf_v"], g["leaf_d"]
+    assert np.linalg.norm(u @ u.T - ur @ ur.T) <= 1e-9
+    assert np.linalg.norm(v @ v.T - vr @ vr.T) <= 1e-9
+    assert np.linalg.norm(d - dr) <= 1e-9 * np.linalg.norm(dr)
+    assert np.linalg.norm(u.T @ u - np.eye(c["r"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "twin" in n and "c3" not in n])
+def test_leaf_bases_contain_true_range_twin(name):
+    """r > k: U is the true rank-k range plus r - k rounding-determined
+    directions (not unique, also in the reference).  The invariant is that
+    span(U) contains the generator's leaf basis."""
+    c = golden_cases.load(name)
+    f = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    truth = c["truth"]
+    L = f.tree.depth
+    for j in (0, (1 << L) - 1):
+        nid = (1 << L) - 1 + j
+        u, v = f.u_bases[nid], f.v_bases[nid]
+        ut, vt = truth.U[L][j], truth.V[L][j]
+        assert np.linalg.norm(ut - u @ (u.T @ ut)) <= 1e-10
+        assert np.linalg.norm(vt - v @ (v.T @ vt)) <= 1e-10
+        assert np.linalg.norm(u.T @ u - np.eye(c["r"])) <= 1e-12
+
+
+def test_dense_sampler_matches_numpy():
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((300, 300))
+    x = rng.standard_normal((300, 77))
+    o = hb.dense_oracle(a)
+    assert rel(o.apply_batch(x), a @ x) <= 1e-14
+    assert rel(o.apply_transpose_batch(x), a.T @ x) <= 1e-14
+    assert o.matvec_count == (77, 77)
+
+
+def test_log_kernel_generator():
+    a = hb.log_kernel_matrix(512).cpu().numpy()
+    assert np.abs(a - O.ellipse_log_kernel(512)).max() <= 1e-13
+
+
+def test_hbs_sampler_matches_oracle_apply():
+    g = O.baseline_generator(333, 24, 4, seed=1)
+    tree = hb.build_tree(333, 24)
+    ub, vb, db = {}, {}, {}
+    for lvl in range(1, tree.depth + 1):
+        for j, nd in enumerate(tree.nodes_at_level(lvl)):
+            ub[nd.id], vb[nd.id], db[nd.id] = g.U[lvl][j], g.V[lvl][j], g.D[lvl][j]
+    f = hb.HbsFactorization(tree, 4, ub, vb, db, g.root)
+    x = O.gaussian(333, 5, 0, 4)
+    assert rel(hb.apply_matrix(f, x), O.apply(g, x)) <= 1e-14
+    assert rel(hb.apply_matrix(f, x, transpose=True), O.apply(g, x, transpose=True)) <= 1e-14
+    o = hb.hbs_oracle(f)
+    assert rel(o.apply_batch(x), O.apply(g, x)) <= 1e-14
+
+
+def test_deterministic_bitwise():
+    c = golden_cases.load("c1_twin")
+    f1 = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    f2 = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    assert np.array_equal(f1.root_disc, f2.root_disc)
+    for lvl in range(1, f1.tree.depth + 1):
+        for a, b in zip(f1.levels[lvl], f2.levels[lvl]):
+            assert torch.equal(a, b)
+
+
+def test_device_resident_samples_match_host_samples():
+    c = golden_cases.load("uneven_333")
+    dev = [torch.from_numpy(m).cuda() for m in c["samples"]]
+    f_host = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
+    f_dev = gpu_compress(dev, c["n"], c["leaf"], c["r"])
+    assert np.array_equal(f_host.root_disc, f_dev.root_disc)
