@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""HBS compress-from-samples throughput on B200 (BASELINE.json metric).
+
+Workload (config 4 of BASELINE.json): exact-rank synthetic HBS, fp64,
+N = 2^20, k = r = 64, leaf 128, s = 192, coupling singular values 0.9^i;
+samples Y = A Omega, Z = A^T Psi from the on-device HBS sampler.  A "step" is
+one full compress_from_samples sweep (all 13 levels + root) of the
+HBM-resident quadruple (6.4 GB, far larger than the 126 MB L2, so no L2
+flush is needed between steps).
+
+  value : rows/s = N / (device time per step), CUDA events, inputs resident
+  e2e   : the public API (SampleSet of pinned host numpy arrays ->
+          compress_from_samples -> factorization materialised on the host)
+  roofline : dominant kernel phase, canonical FP64 flops
+             over its live CUDA-event time, against the measured FP64 peak
+  cpu_baseline : the CPU oracle port of the reference on a bounded sample
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, oracle/hbs_oracle.py -- numerically bitwise-identical to the
+reference) on the host cores instead.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (N, k, leaf, s, r, decay)
+    "c1": (4096, 16, 32, 48, 16, None),
+    "c2": (1 << 16, 32, 64, 96, 32, None),
+    "c4": (1 << 20, 64, 128, 192, 64, 0.9),
+    "c5": (1 << 22, 128, 256, 384, 128, None),
+}
+METRIC = "HBS compress-from-samples rows/s (fp64) at N=2^20,k=64"
+PHASES = ("probe_qr", "panel_factors", "apply_q_solve", "basis_qr", "discrepancy_gemm", "lift_gemm")
+
+
+def canonical_phase_flops(n, s, r):
+    """Canonical Householder flop model per box, by phase."""
+    return {
+        "probe_qr": 2 * (2 * n * n * (s - n / 3)),
+        "panel_factors": 0.0,
+        "apply_q_solve": 2 * ((4 * n * n * s - 2 * n ** 3) + n ** 3),
+        "basis_qr": 2 * (4 * r * r * (n - r / 3)),
+        "discrepancy_gemm": 12 * r * n * n,
+        "lift_gemm": 4 * n * n * s + 8 * r * n * s,
+    }
+
+
+def canonical_total_flops(tree, s, r):
+    total = 0.0
+    for level in range(tree.depth, 0, -1):
+        sizes = tree.level_sizes(level) if level == tree.depth else np.full(1 << level, 2 * r)
+        for n in np.unique(sizes):
+            total += int((sizes == n).sum()) * sum(canonical_phase_flops(int(n), s, r).values())
+    n = 2 * r
+    total += 2 * n * n * (s - n / 3) + 4 * n * n * s - n ** 3
+    return total
+
+
+def fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    with open(path) as fh:
+        return float(json.load(fh)["fp64_peak_tflops"]), "measured: DMMA m8n8k4 microbenchmark " \
+            "(tools/fp64_peak.cu, profiles/fp64_peaks_r01.json; cuBLAS DGEMM 8192^3 = 35.5 TF/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        load = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_rate(cfg, n_sample, repeats=1):
+    """The oracle port of the reference (bitwise-identical numerics) on a
+    bounded sample of the workload: same k, r, leaf, s; N = n_sample."""
+    from oracle import hbs_oracle as O
+    _, k, leaf, s, r, decay = cfg
+    g = O.baseline_generator(n_sample, leaf, k, seed=0, decay=decay)
+    om, ps, y, z = O.samples_from(g, s, 0)
+    rates = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.compress(om, ps, y, z, g.bounds, r)
+        rates.append(n_sample / (time.perf_counter() - t0))
+    return rates
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    n_sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, n_sample)
+    rates = []
+    for _ in range(args.steps):
+        rates += cpu_reference_rate(cfg, n_sample)
+    value = float(np.mean(rates))
+    N = cfg[0]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * N / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args, cfg, world),
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle port of compress_from_samples on the config-4 shape at N={n_sample} "
+                                   f"(rows/s is N-independent at fixed k, leaf, s); numpy/OpenBLAS with "
+                                   f"{cores} threads available, effectively single-core"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, cfg, world):
+    N, k, leaf, s, r, decay = cfg
+    return {"workload": f"{args.config}: exact-rank synthetic HBS, N={N} per GPU, k={k}, r={r}, leaf={leaf}, "
+                        f"s={s}" + (f", coupling decay {decay}" if decay else ""),
+            "N_per_gpu": N, "k": k, "r": r, "leaf": leaf, "s": s, "global_rows": N * world,
+            "parallelism": f"subtree x{world}" if world > 1 else "single GPU",
+            "l2_policy": "inputs (4 x N x s fp64) exceed L2 126 MB; no flush needed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override N (rows per GPU)")
+    ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 15)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    cfg = list(CONFIGS[args.config])
+    if args.n:
+        cfg[0] = args.n
+    cfg = tuple(cfg)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_02990_b200 as hb
+    from paper_2205_02990_b200 import synthetic
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N, k, leaf, s, r, decay = cfg
+    tree = hb.build_tree(N, leaf)
+    t0 = time.perf_counter()
+    gen = synthetic.device_generator(tree, k, seed=rank, decay=decay, device=dev)
+    om, ps, y, z = synthetic.device_samples(gen, s, seed=rank)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    plan = hb.CompressPlan(tree, s, r, device=dev)
+    lib = hb._native.lib()
+
+    for _ in range(args.warmup):
+        plan.run(om, ps, y, z)
+    torch.cuda.synchronize()
+    plan.raise_for_status()
+
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.hbs_launch_counter()
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.run(om, ps, y, z)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = (lib.hbs_launch_counter() - launches0)
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    ms_step = ms_total / args.steps
+    value = N * world / (ms_step / 1e3)
+
+    # accuracy of this run vs the true operator (probe x, 8 columns)
+    xg = torch.Generator(device=dev)
+    xg.manual_seed(4)
+    x = torch.randn(N, 8, generator=xg, dtype=torch.float64, device=dev)
+    f = plan.factorization()
+    err = float(torch.linalg.norm(hb.apply_matrix(f, x) - hb.apply_matrix(gen, x)) /
+                torch.linalg.norm(hb.apply_matrix(gen, x)))
+
+    # roofline: live per-phase CUDA-event timing of one extra sweep
+    peak_tf, peak_src = fp64_peak()
+    phase_ms = {p: 0.0 for p in PHASES}
+    phase_flops = {p: 0.0 for p in PHASES}
+    import ctypes
+    buf = (ctypes.c_float * 6)()
+    quad = (om, ps, y, z)
+    for idx, level in enumerate(range(tree.depth, 0, -1)):
+        g = plan.geometry[level]
+        u, v, d = plan.levels[level]
+        out = plan.lift[idx % 2]
+        rc = lib.hbs_compress_level_profiled(
+            g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.max_rows, s, r, plan.tol,
+            *(m.data_ptr() for m in quad), u.data_ptr(), v.data_ptr(), d.data_ptr(),
+            *(m.data_ptr() for m in out), plan.workspace.data_ptr(), plan.workspace_bytes,
+            plan.status.data_ptr(), stream.cuda_stream, buf)
+        hb._native.check(rc, "profiled level")
+        sizes = np.diff(g.begins_host)
+        for i, p in enumerate(PHASES):
+            phase_ms[p] += buf[i]
+            phase_flops[p] += sum(canonical_phase_flops(int(n), s, r)[p] for n in sizes)
+        quad = tuple(m[:g.nbox * r] for m in out)
+    dom = max(PHASES, key=lambda p: phase_ms[p])
+    achieved = phase_flops[dom] / (phase_ms[dom] / 1e3) / 1e12
+    total_flops = canonical_total_flops(tree, s, r)
+    step_tf = total_flops / (ms_step / 1e3) / 1e12
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        host = [torch.empty(N, s, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+        for h, dsrc in zip(host, quad_src := (om, ps, y, z)):
+            h.copy_(dsrc)
+        samples = hb.SampleSet(*(h.numpy() for h in host))
+        times = []
+        fact_bytes = None
+        for it in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fh = hb.compress_from_samples(samples, tree, hb.CompressionConfig(rank=r, leaf_threshold=leaf))
+            fact_bytes = fh.materialize()
+            dt = time.perf_counter() - t0
+            if it > 0:
+                times.append(dt)
+            del fh
+        e2e = {"value": N / float(np.mean(times)), "unit": "rows/s", "h2d_bytes_per_step": 4 * N * s * 8,
+               "d2h_bytes_per_step": int(fact_bytes), "s_per_step": float(np.mean(times))}
+        del host, samples
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        n_cpu = min(args.cpu_sample, N)
+        t0 = time.perf_counter()
+        rate = cpu_reference_rate(cfg, n_cpu)[0]
+        cpu = {"value": rate, "unit": "rows/s", "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"oracle port of the reference compress_from_samples (bitwise-identical numerics) on the "
+                         f"{args.config} shape at N={n_cpu}; numpy/OpenBLAS, all host threads available, "
+                         f"effectively single-core; {time.perf_counter() - t0:.1f} s incl. input generation"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox generator, seeded)",
+            "config": config_block(args, cfg, world),
+            "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": None, "peak_source": peak_src,
+                         "step_achieved": step_tf, "step_frac": step_tf / peak_tf,
+                         "step_canonical_flops": total_flops,
+                         "phase_ms": phase_ms, "phase_tflops": {p: (phase_flops[p] / (phase_ms[p] / 1e3) / 1e12
+                                                                    if phase_ms[p] > 0 else None) for p in PHASES}},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "accuracy": {"rel_apply_err_vs_truth": err, "probe": "x = N(0,1) N x 8"},
+            "gen_seconds": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

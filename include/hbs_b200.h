@@ -77,6 +77,21 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
                        double* lift_omega, double* lift_psi, double* lift_y, double* lift_z,
                        void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
 
+/* Same as hbs_compress_level, but records CUDA events between its phases and
+ * writes their durations (ms) to the HOST array phase_ms[6]: probe QR,
+ * panel factors, apply-Q + solve, basis QR (col), discrepancy GEMMs, lift
+ * GEMMs.  Synchronises the stream; for measurement only. */
+int hbs_compress_level_profiled(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows,
+                                int s, int r, double tol,
+                                const double* omega, const double* psi, const double* y, const double* z,
+                                double* u, double* v, double* d,
+                                double* lift_omega, double* lift_psi, double* lift_y, double* lift_z,
+                                void* workspace, size_t workspace_bytes, int32_t* status, void* stream,
+                                float* phase_ms);
+
+/* Number of CUDA kernels launched by this library so far (process-wide). */
+unsigned long long hbs_launch_counter(void);
+
 /* Root core D_root = Y_root Omega_root^+ (compress.py:230-233), rows = 2r.
  * `row_begin`/`sq_off` describe the single root box ({0, 2r} / {0, 4r^2}). */
 int hbs_root_workspace_bytes(int rows, int s, size_t* bytes);

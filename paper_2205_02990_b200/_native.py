@@ -32,6 +32,9 @@ SIGNATURES = {
     "hbs_level_workspace_bytes": ([_I64, _I, _I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_compress_level": ([_I64, _P, _P, _I, _I, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                             _P, _SZ, _P, _P], _I),
+    "hbs_compress_level_profiled": ([_I64, _P, _P, _I, _I, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                     _P, _P, _SZ, _P, _P, ctypes.POINTER(ctypes.c_float)], _I),
+    "hbs_launch_counter": ([], ctypes.c_ulonglong),
     "hbs_root_workspace_bytes": ([_I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_compress_root": ([_P, _P, _I, _I, _D, _P, _P, _P, _P, _SZ, _P, _P], _I),
     "hbs_apply_workspace_bytes": ([_I, _I, _I64, ctypes.POINTER(_SZ)], _I),

@@ -235,7 +235,9 @@ def _device_tensor(a, device):
     arr = np.ascontiguousarray(a, dtype=np.float64)
     t = torch.from_numpy(arr)
     if device.type == "cuda":
-        t = t.pin_memory().to(device, non_blocking=True)
+        if not t.is_pinned():
+            t = t.pin_memory()
+        t = t.to(device, non_blocking=True)
     return t
 
 

@@ -129,6 +129,7 @@ static int launch_applyq_tw(const ApplyQArgs& args, int nsides, cudaStream_t str
   cudaFuncSetAttribute(applyq_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((args.n_max + TW - 1) / TW, (unsigned)args.geo.nbox, nsides);
   applyq_kernel<TW><<<grid, 256, smem, stream>>>(args);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 

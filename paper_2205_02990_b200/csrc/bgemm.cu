@@ -141,6 +141,7 @@ int launch_bgemm(const BgemmArgs& args, cudaStream_t stream) {
   if (tiles * args.geo.nbox >= (1ll << 31)) return kErrUnsupported;
   dim3 grid((unsigned)(tiles * args.geo.nbox));
   bgemm_kernel<<<grid, 256, 0, stream>>>(args);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 

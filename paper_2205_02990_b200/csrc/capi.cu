@@ -5,8 +5,38 @@
 #include "../../include/hbs_b200.h"
 #include "kernels.h"
 
+#include <atomic>
+
 namespace hbs {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 namespace {
+
+// Optional per-phase timing of hbs_compress_level (hbs_compress_level_profiled).
+struct PhaseTimer {
+  cudaEvent_t ev[8];
+  int n = 0;
+  bool on = false;
+  cudaStream_t st = nullptr;
+  void start(cudaStream_t s) {
+    on = true; st = s; n = 0;
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[n++], st);
+  }
+  void mark() { if (on && n < 8) cudaEventRecord(ev[n++], st); }
+  void finish(float* out, int nphase) {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 0; i < nphase; ++i) {
+      out[i] = 0.f;
+      if (i + 1 < n) cudaEventElapsedTime(&out[i], ev[i], ev[i + 1]);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    on = false;
+  }
+};
+PhaseTimer g_timer;  // only used by the profiled entry point (not thread-safe by design)
 
 constexpr size_t kAlign = 256;
 
@@ -103,6 +133,7 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
     S.status = status + sd * geo.nbox;
   }
   HBS_TRY(launch_geqrf(g, nsides, st));
+  g_timer.mark();
 
   const int npanel = (nr + kNB - 1) / kNB;
   PanelArgs p;
@@ -117,6 +148,7 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
     S.rinv = w.Rinv[sd]; S.rinv_stride = (int64_t)npanel * kNB * kNB;
   }
   HBS_TRY(launch_panel_factors(p, nsides, st));
+  g_timer.mark();
 
   ApplyQArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -137,7 +169,9 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
       S.yp = w.P[sd]; S.yp_stride = (int64_t)nr * r; S.ldyp = r;
     }
   }
-  return launch_applyq(a, nsides, st);
+  HBS_TRY(launch_applyq(a, nsides, st));
+  g_timer.mark();
+  return kOk;
 }
 
 }  // namespace
@@ -187,6 +221,7 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
   HBS_TRY(launch_geqrf(g, 2, st));
+  g_timer.mark();
 
   // Discrepancy D = X - U [U^T X - U^T W^T + (U^T W^T V) V^T]  (compress.py:192-197)
   const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
@@ -206,6 +241,7 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Xn, w.M4, 0, rs, 0, nr, false, 1.0, -1.0, G1, st));
   HBS_TRY(gemm(geo, dfix(r), drows(), dfix(r), r, nr, M3, Vt, w.M4, 0, rs, 0, nr, false, 1.0, 1.0, M4, st));
   HBS_TRY(gemm(geo, drows(), drows(), dfix(r), nr, nr, Un, M4, d, 0, 0, 1, 0, true, -1.0, 1.0, Xn, st));
+  g_timer.mark();
 
   if (lift_omega) {
     // Parent quadruple rows of child b: [b*r, (b+1)*r)  (compress.py:209-227)
@@ -229,7 +265,24 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E2, Ps, lift_z, 0, prs, 0, s, false, -1.0, 1.0,
                  op(lift_z, 0, prs, 0, s, false, false), st));
   }
+  g_timer.mark();
   return HBS_OK;
+}
+
+unsigned long long hbs_launch_counter(void) { return g_launches.load(); }
+
+int hbs_compress_level_profiled(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows,
+                                int s, int r, double tol, const double* omega, const double* psi,
+                                const double* y, const double* z, double* u, double* v, double* d,
+                                double* lift_omega, double* lift_psi, double* lift_y, double* lift_z,
+                                void* workspace, size_t workspace_bytes, int32_t* status, void* stream,
+                                float* phase_ms) {
+  g_timer.start(static_cast<cudaStream_t>(stream));
+  const int rc = hbs_compress_level(nbox, row_begin, sq_off, max_rows, s, r, tol, omega, psi, y, z, u, v, d,
+                                    lift_omega, lift_psi, lift_y, lift_z, workspace, workspace_bytes, status,
+                                    stream);
+  g_timer.finish(phase_ms, 6);
+  return rc;
 }
 
 int hbs_root_workspace_bytes(int rows, int s, size_t* bytes) {

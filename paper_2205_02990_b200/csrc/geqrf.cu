@@ -291,6 +291,7 @@ int launch_geqrf(GeqrfArgs args, int nsides, cudaStream_t stream) {
       return kErrUnsupported;
   }
 #undef HBS_GEQRF_CASE
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 

@@ -20,6 +20,10 @@ enum Status : int {
 
 constexpr size_t kMaxSmemBytes = 227 * 1024;
 
+// Count of kernels this library has launched (process-wide, for the bench's
+// gpu_launches claim); incremented by every launch_* helper.
+void note_launch();
+
 // ---------------------------------------------------------------- geqrf
 enum GeqrfMode : int { kGeqrfFactor = 0, kGeqrfOrtho = 1 };
 

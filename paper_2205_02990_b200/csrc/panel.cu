@@ -91,6 +91,7 @@ int launch_panel_factors(PanelArgs args, int nsides, cudaStream_t stream) {
     cudaFuncSetAttribute(panel_factors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(npanel, (unsigned)args.geo.nbox, nsides);
   panel_factors_kernel<<<grid, 128, smem, stream>>>(args);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 

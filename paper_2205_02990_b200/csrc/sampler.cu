@@ -29,5 +29,6 @@ extern "C" int hbs_fill_log_kernel(int64_t n, int64_t row0, int64_t rows, double
   if (n < 1 || rows < 0 || row0 < 0 || row0 + rows > n) return HBS_ERR_DIMENSION;
   if (rows == 0) return HBS_OK;
   hbs::fill_log_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(n, row0, rows, a);
+  hbs::note_launch();
   return cudaGetLastError() == cudaSuccess ? HBS_OK : HBS_ERR_CUDA;
 }

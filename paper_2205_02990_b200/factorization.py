@@ -148,6 +148,25 @@ class HbsFactorization:
             self._host[key] = t.cpu().numpy()
         return self._host[key]
 
+    def materialize(self) -> int:
+        """Copy every block to pinned host memory (one stream, one sync) so the
+        reference-style dict views are free afterwards.  Returns bytes copied."""
+        pending, nbytes = [], 0
+        for level in range(1, self.tree.depth + 1):
+            for kind, t in zip("uvd", self.levels[level]):
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t, non_blocking=True)
+                pending.append(((level, kind), h))
+                nbytes += t.numel() * 8
+        root = torch.empty(self.root_device.shape, dtype=torch.float64, pin_memory=True)
+        root.copy_(self.root_device, non_blocking=True)
+        nbytes += root.numel() * 8
+        torch.cuda.synchronize(self.device)
+        for key, h in pending:
+            self._host[key] = h.numpy()
+        self._host["root"] = root.numpy()
+        return nbytes
+
     def validate(self):
         """Orthonormality of every basis and finiteness of all blocks
         (factorization.py:69-86), evaluated on the device per level."""
