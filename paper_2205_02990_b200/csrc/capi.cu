@@ -84,10 +84,10 @@ size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bo
   } else {
     w.G1 = w.M3 = w.M4 = w.E1 = w.E2 = nullptr;
   }
-  const bool big_factor = geqrf_smem_bytes(s, nr, kGeqrfFactor) > kMaxSmemBytes;
-  const bool big_ortho = geqrf_smem_bytes(nr, r, kGeqrfOrtho) > kMaxSmemBytes;
+  const bool big_factor = !hqr_fits_smem(s, nr, kGeqrfFactor);
+  const bool big_ortho = !root_only && !hqr_fits_smem(nr, r, kGeqrfOrtho);
   w.gscratch = (big_factor || big_ortho)
-                   ? c.take<double>(geqrf_scratch_doubles(s > nr ? s : nr, nr > r ? nr : r, nbox))
+                   ? c.take<double>(hqr_scratch_doubles(s > nr ? s : nr, nr > r ? nr : r, nbox))
                    : nullptr;
   return c.used + kAlign;
 }
@@ -124,31 +124,20 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
   g.m_fixed = s; g.m_is_rows = 0; g.n_fixed = 0; g.n_is_rows = 1;
   g.m_max = s; g.n_max = nr; g.tol = tol; g.gscratch = w.gscratch;
   const double* oms[2] = {om0, om1};
+  const int npanel = (nr + kNB - 1) / kNB;
   for (int sd = 0; sd < nsides; ++sd) {
     GeqrfSide& S = g.side[sd];
     S.src = oms[sd]; S.src_c_rb = s; S.src_c_b = 0; S.src_rs = 1; S.src_cs = s;
     S.vt = w.vt[sd]; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
     S.r = w.R[sd]; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
     S.tau = w.tau[sd]; S.tau_stride = nr;
-    S.status = status + sd * geo.nbox;
-  }
-  HBS_TRY(launch_geqrf(g, nsides, st));
-  g_timer.mark();
-
-  const int npanel = (nr + kNB - 1) / kNB;
-  PanelArgs p;
-  std::memset(&p, 0, sizeof(p));
-  p.geo = geo; p.m = s; p.n_fixed = 0; p.n_is_rows = 1; p.n_max = nr;
-  for (int sd = 0; sd < nsides; ++sd) {
-    PanelSide& S = p.side[sd];
-    S.vt = w.vt[sd]; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
-    S.r = w.R[sd]; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
-    S.tau = w.tau[sd]; S.tau_stride = nr;
     S.t = w.T[sd]; S.t_stride = (int64_t)npanel * kNB * kNB;
     S.rinv = w.Rinv[sd]; S.rinv_stride = (int64_t)npanel * kNB * kNB;
+    S.status = status + sd * geo.nbox;
   }
-  HBS_TRY(launch_panel_factors(p, nsides, st));
+  HBS_TRY(launch_hqr(g, nsides, st));
   g_timer.mark();
+  g_timer.mark();  // (panel factors are produced inside the QR kernel)
 
   ApplyQArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -220,7 +209,7 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     S.src = w.P[sd]; S.src_c_rb = 0; S.src_c_b = (int64_t)nr * r; S.src_rs = r; S.src_cs = 1;
     S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
-  HBS_TRY(launch_geqrf(g, 2, st));
+  HBS_TRY(launch_hqr(g, 2, st));
   g_timer.mark();
 
   // Discrepancy D = X - U [U^T X - U^T W^T + (U^T W^T V) V^T]  (compress.py:192-197)

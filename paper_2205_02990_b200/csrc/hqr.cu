@@ -1,0 +1,486 @@
+// Batched blocked Householder QR of small fp64 matrices (one CTA per matrix).
+//
+// Restates the reference's LAPACK path: numpy.linalg.qr -> dgeqrf (blocked,
+// dlarfg reflectors, dlarft compact-WY T, dlarfb trailing update) and dorgqr,
+// used by `nullspace` (linalg.py:52-62: complete Q of Omega_tau^T, last r
+// columns) and `col` (linalg.py:35-49: reduced Q of Y_tau P).  The reflectors
+// are the LAPACK ones, so the "last r columns" null-space subspace agrees with
+// the reference when nullity > r.
+//
+// Structure per 32-column panel (512 threads, 16 warps):
+//   * panel factorisation: each warp owns two panel columns in registers; one
+//     __syncthreads per column; the compact-WY dots v_c . v_j are formed in the
+//     same shuffle reductions as the column updates;
+//   * T (dlarft recurrence) and R's diagonal-block inverse by two warps;
+//   * trailing update A <- (I - V T^T V^T) A on the FP64 tensor cores
+//     (DMMA m8n8k4), one 8-column strip per warp, W kept in registers and
+//     re-laid out C-fragment -> B-fragment with shuffles.
+// kOrtho then forms Q = H_0 ... H_{n-1} [I; 0] block-backward (dorgqr) with
+// the same tensor-core block-reflector routine.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hbs {
+
+namespace {
+
+constexpr int kP = 32;        // panel width (== kNB)
+constexpr int kLdT = kP + 1;  // T / G smem leading dimension
+
+struct Reflector {  // dlarfg for the current pivot
+  double tau, beta, scale;
+};
+
+HBS_DEV Reflector make_reflector(double alpha, double xn2) {
+  Reflector h{0.0, alpha, 0.0};
+  if (xn2 != 0.0) {  // beta = -sign(alpha) * hypot(alpha, ||x||)
+    h.beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+    h.tau = (h.beta - alpha) / h.beta;
+    h.scale = 1.0 / (alpha - h.beta);
+  }
+  return h;
+}
+
+// V(i, q) of panel j0: unit lower trapezoidal, stored in A's panel columns
+// (tails already scaled).  q >= nbp -> 0.
+HBS_DEV double vval(const double* A, int lda, int j0, int nbp, int i, int q) {
+  const int c = j0 + q;
+  if (q >= nbp || i < c) return 0.0;
+  return i == c ? 1.0 : A[i + c * lda];
+}
+
+// Fetch W(p, g) (p = kk + t) from C-fragments acc[f][e] (row g', col 2t'+e)
+// into the B-fragment layout (row t, col g) of k-step kk.
+template <int NF>
+HBS_DEV double cfrag_to_bfrag(const double (&acc)[NF][2], int kk, int lane) {
+  // kk is a compile-time constant in every (unrolled) caller, so acc[kk >> 3]
+  // resolves to registers and only two shuffles are issued.
+  const int g = lane >> 2, t = lane & 3;
+  const int src = 4 * ((kk & 7) + t) + (g >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, acc[kk >> 3][0], src);
+  const double v1 = __shfl_sync(0xffffffffu, acc[kk >> 3][1], src);
+  return (g & 1) ? v1 : v0;
+}
+
+// A(j0:m, cb:ce) <- (I - V op(T) V^T) A(j0:m, cb:ce), V = panel j0 (nbp cols),
+// op(T) = T^T when trans (dgeqrf trailing update, H^T from the left), else T
+// (dorgqr).  T in smem (kP x kLdT).  mpad = rows rounded up to 8 (zero rows).
+HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp, const double* T, bool trans,
+                                   int cb, int ce) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nstrip = (ce - cb + 7) >> 3;
+  for (int sidx = warp; sidx < nstrip; sidx += nw) {
+    const int c0 = cb + 8 * sidx;
+    const bool colok = c0 + g < ce;
+    // GEMM1: W = V^T A_strip  (32 x 8), K = rows j0 .. mpad
+    double w[4][2] = {};
+    for (int k = j0; k < mpad; k += 4) {
+      const double bv = colok ? A[(k + t) + (c0 + g) * lda] : 0.0;
+      if (k < j0 + kP) {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) dmma8x8x4(w[f][0], w[f][1], vval(A, lda, j0, nbp, k + t, 8 * f + g), bv);
+      } else {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const double av = (8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0;
+          dmma8x8x4(w[f][0], w[f][1], av, bv);
+        }
+      }
+    }
+    // GEMM2: W2 = op(T) W (32 x 8)
+    double w2[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const double bv = cfrag_to_bfrag<4>(w, kk, lane);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int row = 8 * f + g, col = kk + t;
+        const double av = trans ? T[col * kLdT + row] : T[row * kLdT + col];
+        dmma8x8x4(w2[f][0], w2[f][1], av, bv);
+      }
+    }
+    double bneg[kP / 4];
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) bneg[kk / 4] = -cfrag_to_bfrag<4>(w2, kk, lane);
+    // GEMM3: A_strip -= V W2, 8-row blocks
+    const int col0 = c0 + 2 * t;
+    const bool ok0 = col0 < ce, ok1 = col0 + 1 < ce;
+    for (int i0 = j0; i0 < mpad; i0 += 8) {
+      const int i = i0 + g;
+      double c0v = ok0 ? A[i + col0 * lda] : 0.0;
+      double c1v = ok1 ? A[i + (col0 + 1) * lda] : 0.0;
+      if (i0 < j0 + kP) {
+#pragma unroll
+        for (int kk = 0; kk < kP; kk += 4) dmma8x8x4(c0v, c1v, vval(A, lda, j0, nbp, i, kk + t), bneg[kk / 4]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kP; kk += 4) {
+          const double av = (kk + t < nbp) ? A[i + (j0 + kk + t) * lda] : 0.0;
+          dmma8x8x4(c0v, c1v, av, bneg[kk / 4]);
+        }
+      }
+      if (ok0) A[i + col0 * lda] = c0v;
+      if (ok1) A[i + (col0 + 1) * lda] = c1v;
+    }
+  }
+}
+
+// Factor panel j0 (nbp <= 32 columns) in place.  Leaves: pre-scale reflector
+// values in A (finalised afterwards by the caller), tau/scale/beta in smem,
+// G(c, j) = v_c . v_j (c < j) in G.
+template <int MR>
+HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                          double* s_beta, double* s_norm, double* G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
+  const int ca = j0 + warp, cb = j0 + warp + nw;
+  const bool own_a = warp < nbp, own_b = warp + nw < nbp;
+  double xa[MR], xb[MR];
+#pragma unroll
+  for (int k = 0; k < MR; ++k) {
+    const int row = j0 + lane + 32 * k;
+    xa[k] = (own_a && k < kc) ? A[row + ca * lda] : 0.0;
+    xb[k] = (own_b && k < kc) ? A[row + cb * lda] : 0.0;
+  }
+  if (warp == 0) {
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int row = j0 + lane + 32 * k;
+      if (k < kc && row > j0) p = fma(xa[k], xa[k], p);
+    }
+    p = warp_sum(p);
+    if (lane == 0) s_norm[0] = p;
+  }
+  __syncthreads();
+  for (int j = 0; j < nbp; ++j) {
+    const int jj = j0 + j;
+    const Reflector h = make_reflector(A[jj + jj * lda], s_norm[j & 1]);
+    const int kj = j >> 5, lj = j & 31;  // register slot of row jj
+    double pv[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int row = j0 + lane + 32 * k;
+      pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+    }
+    // row-jj entries of my columns
+    double ra = 0.0, rb = 0.0;
+#pragma unroll
+    for (int k = 0; k < MR; ++k)
+      if (k == kj) { ra = xa[k]; rb = xb[k]; }
+    ra = __shfl_sync(0xffffffffu, ra, lj);
+    rb = __shfl_sync(0xffffffffu, rb, lj);
+    double da = 0.0, db = 0.0;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      da = fma(pv[k], xa[k], da);
+      db = fma(pv[k], xb[k], db);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      da += __shfl_xor_sync(0xffffffffu, da, o);
+      db += __shfl_xor_sync(0xffffffffu, db, o);
+    }
+    // column a
+    if (own_a && ca > jj) {
+      const double f = h.tau * (ra + h.scale * da), gs = f * h.scale;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) xa[k] = fma(-gs, pv[k], xa[k]);
+      if (lane == lj) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (k == kj) xa[k] -= f;
+      }
+    } else if (own_a && ca < jj && lane == 0) {
+      G[(ca - j0) * kLdT + j] = s_scale[ca] * (ra + h.scale * da);
+    }
+    if (own_b && cb > jj) {
+      const double f = h.tau * (rb + h.scale * db), gs = f * h.scale;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) xb[k] = fma(-gs, pv[k], xb[k]);
+      if (lane == lj) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (k == kj) xb[k] -= f;
+      }
+    } else if (own_b && cb < jj && lane == 0) {
+      G[(cb - j0) * kLdT + j] = s_scale[cb] * (rb + h.scale * db);
+    }
+    // the next pivot's owner publishes it (column + norm of rows > jj+1)
+    const int nxt = jj + 1;
+    if (j + 1 < nbp && (ca == nxt || cb == nxt)) {
+      const bool isa = (ca == nxt);
+      double p = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = j0 + lane + 32 * k;
+        const double x = isa ? xa[k] : xb[k];
+        if (k < kc) {
+          A[row + nxt * lda] = x;
+          if (row > nxt) p = fma(x, x, p);
+        }
+      }
+      p = warp_sum(p);
+      if (lane == 0) s_norm[(j + 1) & 1] = p;
+    }
+    if (threadIdx.x == 0) {
+      s_tau[jj] = h.tau;
+      s_scale[jj] = h.scale;
+      s_beta[jj] = h.beta;
+    }
+    __syncthreads();
+  }
+  // write back the owned columns (final values, reflector tails unscaled)
+#pragma unroll
+  for (int k = 0; k < MR; ++k) {
+    const int row = j0 + lane + 32 * k;
+    if (k < kc) {
+      if (own_a) A[row + ca * lda] = xa[k];
+      if (own_b) A[row + cb * lda] = xb[k];
+    }
+  }
+  __syncthreads();
+  // finalise: v tails = x * scale, diagonal = beta
+  for (int e = threadIdx.x; e < nbp * (m - j0); e += blockDim.x) {
+    const int q = e / (m - j0), i = j0 + e % (m - j0);
+    const int c = j0 + q;
+    if (i > c) A[i + c * lda] *= s_scale[c];
+    else if (i == c) A[i + c * lda] = s_beta[c];
+  }
+  __syncthreads();
+}
+
+// T (dlarft forward/columnwise) from G and tau, by warp 0: lane a owns row a.
+HBS_DEV void form_t(double* T, const double* G, const double* s_tau, int j0, int nbp) {
+  const int lane = threadIdx.x & 31, a = lane;
+  for (int c = 0; c < kP; ++c) {
+    const double tc = (c < nbp) ? s_tau[j0 + c] : 0.0;
+    double acc = 0.0;
+    for (int q = a; q < c; ++q) acc = fma(T[a * kLdT + q], G[q * kLdT + c], acc);
+    T[a * kLdT + c] = (a < c) ? -tc * acc : (a == c ? tc : 0.0);
+    __syncwarp();
+  }
+}
+
+// Inverse of R's diagonal block (panel j0), by one warp: lane c solves R x = e_c.
+HBS_DEV void diag_block_inverse(const double* A, int lda, int j0, int nbp, double* out) {
+  const int c = threadIdx.x & 31;
+  double x[kP];
+#pragma unroll
+  for (int i = kP - 1; i >= 0; --i) {
+    double acc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = i + 1; k < kP; ++k) {
+      const double rik = (i < nbp && k < nbp) ? A[(j0 + i) + (j0 + k) * lda] : 0.0;
+      acc = fma(-rik, x[k], acc);
+    }
+    const double rii = (i < nbp) ? A[(j0 + i) + (j0 + i) * lda] : 1.0;
+    x[i] = acc / rii;
+  }
+#pragma unroll
+  for (int i = 0; i < kP; ++i) out[i * kP + c] = x[i];
+}
+
+}  // namespace
+
+template <int MR, bool SMEM>
+__global__ void __launch_bounds__(512) hqr_kernel(GeqrfArgs args) {
+  extern __shared__ double smem[];
+  const int side = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const GeqrfSide& S = args.side[side];
+  const int nb = box_rows(args.geo, b);
+  const int m = args.m_is_rows ? nb : args.m_fixed;
+  const int n = args.n_is_rows ? nb : args.n_fixed;
+  const int lda = args.lda_max;
+  const int mpad = round_up(m, 32);
+  const int npanel = (n + kP - 1) / kP;
+  const int64_t rb = args.geo.row_begin[b];
+
+  // smem: small vectors | T / G (per panel in ortho mode) | A (if SMEM)
+  double* s_tau = smem;
+  double* s_scale = s_tau + args.n_max;
+  double* s_beta = s_scale + args.n_max;
+  double* s_norm = s_beta + args.n_max;
+  double* G = smem + round_up(3 * args.n_max + 2, 2);
+  double* Tbase = G + kP * kLdT;
+  const int tslots = (args.mode == kGeqrfOrtho) ? (args.n_max + kP - 1) / kP : 1;
+  double* A = SMEM ? Tbase + (size_t)round_up(kP * kLdT * tslots, 2)
+                   : args.gscratch + ((size_t)side * args.geo.nbox + b) * (size_t)lda * args.n_max;
+
+  // load, zero-padding rows m .. mpad-1
+  const double* src = S.src + S.src_c_rb * rb + S.src_c_b * b;
+  if (S.src_rs == 1) {
+    for (int e = threadIdx.x; e < mpad * n; e += blockDim.x) {
+      const int j = e / mpad, i = e % mpad;
+      A[i + j * lda] = (i < m) ? src[(int64_t)i + (int64_t)j * S.src_cs] : 0.0;
+    }
+  } else {
+    for (int e = threadIdx.x; e < mpad * n; e += blockDim.x) {
+      const int i = e / n, j = e % n;
+      A[i + j * lda] = (i < m) ? src[(int64_t)i * S.src_rs + (int64_t)j * S.src_cs] : 0.0;
+    }
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5;
+  for (int p = 0; p < npanel; ++p) {
+    const int j0 = p * kP, nbp = min(kP, n - j0);
+    double* T = Tbase + (args.mode == kGeqrfOrtho ? p * kP * kLdT : 0);
+    panel_factor<MR>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_norm, G);
+    if (warp == 0) {
+      form_t(T, G, s_tau, j0, nbp);
+    } else if (warp == 1 && args.mode == kGeqrfFactor) {
+      diag_block_inverse(A, lda, j0, nbp, S.rinv + (size_t)b * S.rinv_stride + (size_t)p * kP * kP);
+    }
+    __syncthreads();
+    if (args.mode == kGeqrfFactor) {
+      double* tout = S.t + (size_t)b * S.t_stride + (size_t)p * kP * kP;
+      for (int e = threadIdx.x; e < kP * kP; e += blockDim.x) tout[e] = T[(e / kP) * kLdT + e % kP];
+    }
+    if (j0 + kP < n) block_reflector_apply(A, lda, round_up(m, 8), j0, nbp, T, true, j0 + kP, n);
+    __syncthreads();
+  }
+
+  if (args.mode == kGeqrfFactor) {
+    if (threadIdx.x < 32) {  // sigma screen on diag(R)
+      double lo = INFINITY, hi = 0.0;
+      for (int j = threadIdx.x; j < n; j += 32) {
+        const double d = fabs(A[j + j * lda]);
+        lo = fmin(lo, d);
+        hi = fmax(hi, d);
+      }
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      if (threadIdx.x == 0) {
+        const bool bad = !(hi > 0.0) || lo < args.tol * hi || !isfinite(hi);
+        S.status[b] = bad ? kBoxIllConditioned : kBoxOk;
+      }
+    }
+    double* vt = S.vt + (size_t)b * S.vt_stride;
+    for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
+      const int j = e / m, i = e % m;
+      vt[(size_t)j * S.ldvt + i] = (i < j) ? 0.0 : (i == j ? 1.0 : A[i + j * lda]);
+    }
+    double* R = S.r + (size_t)b * S.r_stride;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, c = e % n;
+      R[(size_t)i * S.ldr + c] = (i <= c) ? A[i + c * lda] : 0.0;
+    }
+    double* tau = S.tau + (size_t)b * S.tau_stride;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) tau[j] = s_tau[j];
+    return;
+  }
+
+  // kOrtho: Q = H_0 ... H_{n-1} [I; 0], panels backwards (dorgqr).
+  const int mp8 = round_up(m, 8);
+  for (int p = npanel - 1; p >= 0; --p) {
+    const int j0 = p * kP, nbp = min(kP, n - j0);
+    const double* T = Tbase + p * kP * kLdT;
+    // columns right of the panel already hold Q; apply the block reflector
+    if (j0 + kP < n) block_reflector_apply(A, lda, mp8, j0, nbp, T, false, j0 + kP, n);
+    // S = T V1^T (nbp x nbp) -> G, where V1 = V(j0:j0+nbp, :)
+    if (warp == 0) {
+      const int a = threadIdx.x & 31;
+      for (int c = 0; c < kP; ++c) {
+        double acc = 0.0;
+        for (int q = 0; q < kP; ++q) acc = fma(T[a * kLdT + q], vval(A, lda, j0, nbp, j0 + c, q), acc);
+        G[a * kLdT + c] = acc;
+      }
+    }
+    __syncthreads();
+    // panel columns: Q(i, j0+c) = delta(i, j0+c) - sum_q V(i, q) S(q, c), i >= j0; 0 above.
+    // Two passes (compute, sync, write) because V lives in the same columns.
+    const int rows = mp8 - j0;
+    constexpr int kMaxPer = 16;  // values per thread per pass
+    for (int base = 0; base < rows * nbp; base += blockDim.x * kMaxPer) {
+      double vals[kMaxPer];
+#pragma unroll
+      for (int u = 0; u < kMaxPer; ++u) {
+        const int e = base + threadIdx.x + u * blockDim.x;
+        vals[u] = 0.0;
+        if (e < rows * nbp) {
+          const int c = e / rows, i = j0 + e % rows;
+          double acc = (i == j0 + c) ? 1.0 : 0.0;
+          for (int q = 0; q < nbp; ++q) acc = fma(-vval(A, lda, j0, nbp, i, q), G[q * kLdT + c], acc);
+          vals[u] = acc;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kMaxPer; ++u) {
+        const int e = base + threadIdx.x + u * blockDim.x;
+        if (e < rows * nbp) {
+          const int c = e / rows, i = j0 + e % rows;
+          A[i + (j0 + c) * lda] = vals[u];
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < j0 * nbp; e += blockDim.x) {
+      const int c = e / j0, i = e % j0;
+      A[i + (j0 + c) * lda] = 0.0;
+    }
+    __syncthreads();
+  }
+  double* q = S.q + S.q_c_rb * rb + S.q_c_b * b;
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    q[(size_t)i * S.ldq + j] = A[i + j * lda];
+  }
+}
+
+size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix) {
+  const int lda = frag_ld(round_up(m_max, 32));
+  const int np = (mode == kGeqrfOrtho) ? (n_max + kP - 1) / kP : 1;
+  size_t d = round_up(3 * n_max + 2, 2) + kP * kLdT + round_up(kP * kLdT * np, 2);
+  if (with_matrix) d += (size_t)lda * n_max;
+  return d * sizeof(double);
+}
+
+size_t hqr_scratch_doubles(int m_max, int n_max, int64_t nbox) {
+  return 2 * (size_t)nbox * (size_t)frag_ld(round_up(m_max, 32)) * n_max;
+}
+
+bool hqr_fits_smem(int m_max, int n_max, int mode) {
+  return hqr_smem_bytes(m_max, n_max, mode, true) <= kMaxSmemBytes;
+}
+
+template <int MR>
+static int launch_hqr_mr(GeqrfArgs& args, int nsides, cudaStream_t stream) {
+  args.lda_max = frag_ld(round_up(args.m_max, 32));
+  const bool fits = hqr_fits_smem(args.m_max, args.n_max, args.mode);
+  if (!fits && args.gscratch == nullptr) return kErrWorkspace;
+  const size_t smem = hqr_smem_bytes(args.m_max, args.n_max, args.mode, fits);
+  dim3 grid((unsigned)args.geo.nbox, nsides);
+  if (fits) {
+    cudaFuncSetAttribute(hqr_kernel<MR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hqr_kernel<MR, true><<<grid, 512, smem, stream>>>(args);
+  } else {
+    cudaFuncSetAttribute(hqr_kernel<MR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hqr_kernel<MR, false><<<grid, 512, smem, stream>>>(args);
+  }
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream) {
+  const int mr = (args.m_max + 31) / 32;
+  switch (mr) {
+    case 1: return launch_hqr_mr<1>(args, nsides, stream);
+    case 2: return launch_hqr_mr<2>(args, nsides, stream);
+    case 3: return launch_hqr_mr<3>(args, nsides, stream);
+    case 4: return launch_hqr_mr<4>(args, nsides, stream);
+    case 5: return launch_hqr_mr<5>(args, nsides, stream);
+    case 6: return launch_hqr_mr<6>(args, nsides, stream);
+    case 7: return launch_hqr_mr<7>(args, nsides, stream);
+    case 8: return launch_hqr_mr<8>(args, nsides, stream);
+    case 9: case 10: return launch_hqr_mr<10>(args, nsides, stream);
+    case 11: case 12: return launch_hqr_mr<12>(args, nsides, stream);
+    case 13: case 14: case 15: case 16: return launch_hqr_mr<16>(args, nsides, stream);
+    default: return kErrUnsupported;
+  }
+}
+
+}  // namespace hbs

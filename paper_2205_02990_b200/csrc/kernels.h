@@ -36,6 +36,8 @@ struct GeqrfSide {
   double* vt; int64_t vt_stride; int ldvt;
   double* r; int64_t r_stride; int ldr;
   double* tau; int64_t tau_stride;
+  double* t; int64_t t_stride;        // hqr: npanel x 32 x 32 compact-WY T blocks
+  double* rinv; int64_t rinv_stride;  // hqr: npanel x 32 x 32 inverses of R's diagonal blocks
   int32_t* status;
   // kOrtho output: q + q_c_rb*row_begin[b] + q_c_b*b, row-major, ld = ldq
   double* q; int64_t q_c_rb, q_c_b; int ldq;
@@ -55,6 +57,13 @@ struct GeqrfArgs {
 size_t geqrf_smem_bytes(int m_max, int n_max, int mode);
 size_t geqrf_scratch_doubles(int m_max, int n_max, int64_t nbox);
 int launch_geqrf(GeqrfArgs args, int nsides, cudaStream_t stream);
+
+// Blocked Householder (hqr.cu): kFactor also emits the per-panel T and R
+// diagonal-block inverses (PanelSide layout) through GeqrfSide::t / rinv.
+size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix);
+size_t hqr_scratch_doubles(int m_max, int n_max, int64_t nbox);
+bool hqr_fits_smem(int m_max, int n_max, int mode);
+int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- panel factors
 // Per (box, side, panel): compact-WY T block (dlarft, forward/columnwise) of
