@@ -23,14 +23,6 @@ HBS_DEV int64_t op_off(const BOperand& o, const LevelGeo& g, int64_t b) {
   return off;
 }
 
-HBS_DEV void cp_async8(double* dst, const double* src, bool pred) {
-  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  const int bytes = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(bytes));
-}
-HBS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-HBS_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 }  // namespace
 
 __global__ void __launch_bounds__(256) bgemm_kernel(BgemmArgs args) {

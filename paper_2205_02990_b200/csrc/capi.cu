@@ -158,7 +158,8 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
       S.yp = w.P[sd]; S.yp_stride = (int64_t)nr * r; S.ldyp = r;
     }
   }
-  HBS_TRY(launch_applyq(a, nsides, st));
+  if (applyq2_smem_bytes(s) <= kMaxSmemBytes) HBS_TRY(launch_applyq2(a, nsides, st));
+  else HBS_TRY(launch_applyq(a, nsides, st));
   g_timer.mark();
   return kOk;
 }

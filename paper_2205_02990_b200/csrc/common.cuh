@@ -64,4 +64,26 @@ inline __host__ __device__ int frag_ld(int cols) {
 
 inline __host__ __device__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// cp.async (LDGSTS) helpers: 8-byte element copies with zero fill.
+HBS_DEV void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(pred ? 8 : 0));
+}
+HBS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+HBS_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// C-fragment (row g, cols 2t, 2t+1 of 8x8 block f) -> A-fragment (row g, col
+// kk + t) of the same row block, for k-step kk of a K = 8*NF operand held as
+// NF C-fragments.  Pure quad shuffles (lanes sharing g).
+template <int NF>
+HBS_DEV double cfrag_to_afrag(const double (&acc)[NF][2], int kk, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int col = (kk & 7) + t;
+  const int src = 4 * g + (col >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, acc[kk >> 3][0], src);
+  const double v1 = __shfl_sync(0xffffffffu, acc[kk >> 3][1], src);
+  return (col & 1) ? v1 : v0;
+}
+
 }  // namespace hbs

@@ -136,6 +136,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
   const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
   const int ca = j0 + warp, cb = j0 + warp + nw;
   const bool own_a = warp < nbp, own_b = warp + nw < nbp;
+  const int clast = own_b ? cb : (own_a ? ca : -1);   // my last owned column
   double xa[MR], xb[MR];
 #pragma unroll
   for (int k = 0; k < MR; ++k) {
@@ -143,7 +144,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
     xa[k] = (own_a && k < kc) ? A[row + ca * lda] : 0.0;
     xb[k] = (own_b && k < kc) ? A[row + cb * lda] : 0.0;
   }
-  if (warp == 0) {
+  if (warp == 0) {  // reflector of the first pivot (column j0, row j0 at lane 0 / slot 0)
     double p = 0.0;
 #pragma unroll
     for (int k = 0; k < MR; ++k) {
@@ -151,83 +152,81 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
       if (k < kc && row > j0) p = fma(xa[k], xa[k], p);
     }
     p = warp_sum(p);
-    if (lane == 0) s_norm[0] = p;
+    const double alpha = __shfl_sync(0xffffffffu, xa[0], 0);
+    if (lane == 0) {
+      const Reflector h = make_reflector(alpha, p);
+      s_norm[0] = h.tau; s_norm[1] = h.scale; s_norm[2] = h.beta;
+    }
   }
   __syncthreads();
   for (int j = 0; j < nbp; ++j) {
     const int jj = j0 + j;
-    const Reflector h = make_reflector(A[jj + jj * lda], s_norm[j & 1]);
-    const int kj = j >> 5, lj = j & 31;  // register slot of row jj
-    double pv[MR];
-#pragma unroll
-    for (int k = 0; k < MR; ++k) {
-      const int row = j0 + lane + 32 * k;
-      pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+    const double* sn = s_norm + 3 * (j & 1);
+    const double tau = sn[0], scale = sn[1];
+    if (threadIdx.x == 0) {
+      s_tau[jj] = tau;
+      s_scale[jj] = scale;
+      s_beta[jj] = sn[2];
     }
-    // row-jj entries of my columns
-    double ra = 0.0, rb = 0.0;
-#pragma unroll
-    for (int k = 0; k < MR; ++k)
-      if (k == kj) { ra = xa[k]; rb = xb[k]; }
-    ra = __shfl_sync(0xffffffffu, ra, lj);
-    rb = __shfl_sync(0xffffffffu, rb, lj);
-    double da = 0.0, db = 0.0;
-#pragma unroll
-    for (int k = 0; k < MR; ++k) {
-      da = fma(pv[k], xa[k], da);
-      db = fma(pv[k], xb[k], db);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      da += __shfl_xor_sync(0xffffffffu, da, o);
-      db += __shfl_xor_sync(0xffffffffu, db, o);
-    }
-    // column a
-    if (own_a && ca > jj) {
-      const double f = h.tau * (ra + h.scale * da), gs = f * h.scale;
-#pragma unroll
-      for (int k = 0; k < MR; ++k) xa[k] = fma(-gs, pv[k], xa[k]);
-      if (lane == lj) {
-#pragma unroll
-        for (int k = 0; k < MR; ++k)
-          if (k == kj) xa[k] -= f;
-      }
-    } else if (own_a && ca < jj && lane == 0) {
-      G[(ca - j0) * kLdT + j] = s_scale[ca] * (ra + h.scale * da);
-    }
-    if (own_b && cb > jj) {
-      const double f = h.tau * (rb + h.scale * db), gs = f * h.scale;
-#pragma unroll
-      for (int k = 0; k < MR; ++k) xb[k] = fma(-gs, pv[k], xb[k]);
-      if (lane == lj) {
-#pragma unroll
-        for (int k = 0; k < MR; ++k)
-          if (k == kj) xb[k] -= f;
-      }
-    } else if (own_b && cb < jj && lane == 0) {
-      G[(cb - j0) * kLdT + j] = s_scale[cb] * (rb + h.scale * db);
-    }
-    // the next pivot's owner publishes it (column + norm of rows > jj+1)
-    const int nxt = jj + 1;
-    if (j + 1 < nbp && (ca == nxt || cb == nxt)) {
-      const bool isa = (ca == nxt);
-      double p = 0.0;
+    if (clast >= 0) {   // warps whose columns are all retired still do the T dots
+      double pv[MR];
 #pragma unroll
       for (int k = 0; k < MR; ++k) {
         const int row = j0 + lane + 32 * k;
-        const double x = isa ? xa[k] : xb[k];
-        if (k < kc) {
-          A[row + nxt * lda] = x;
-          if (row > nxt) p = fma(x, x, p);
+        pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+      }
+      // row jj lives in slot 0 of lane j
+      const double ra = __shfl_sync(0xffffffffu, xa[0], j);
+      const double rb = __shfl_sync(0xffffffffu, xb[0], j);
+      double da = 0.0, db = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        da = fma(pv[k], xa[k], da);
+        db = fma(pv[k], xb[k], db);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        da += __shfl_xor_sync(0xffffffffu, da, o);
+        db += __shfl_xor_sync(0xffffffffu, db, o);
+      }
+      if (own_a && ca > jj) {
+        const double f = tau * (ra + scale * da), gs = f * scale;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) xa[k] = fma(-gs, pv[k], xa[k]);
+        if (lane == j) xa[0] -= f;
+      } else if (own_a && ca < jj && lane == 0) {
+        G[(ca - j0) * kLdT + j] = s_scale[ca] * (ra + scale * da);
+      }
+      if (own_b && cb > jj) {
+        const double f = tau * (rb + scale * db), gs = f * scale;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) xb[k] = fma(-gs, pv[k], xb[k]);
+        if (lane == j) xb[0] -= f;
+      } else if (own_b && cb < jj && lane == 0) {
+        G[(cb - j0) * kLdT + j] = s_scale[cb] * (rb + scale * db);
+      }
+      // the next pivot's owner publishes column, norm and reflector
+      const int nxt = jj + 1;
+      if (j + 1 < nbp && (ca == nxt || cb == nxt)) {
+        const bool isa = (ca == nxt);
+        double p = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          const int row = j0 + lane + 32 * k;
+          const double x = isa ? xa[k] : xb[k];
+          if (k < kc) {
+            A[row + nxt * lda] = x;
+            if (row > nxt) p = fma(x, x, p);
+          }
+        }
+        p = warp_sum(p);
+        const double alpha = __shfl_sync(0xffffffffu, isa ? xa[0] : xb[0], j + 1);
+        if (lane == 0) {
+          const Reflector h = make_reflector(alpha, p);
+          double* so = s_norm + 3 * ((j + 1) & 1);
+          so[0] = h.tau; so[1] = h.scale; so[2] = h.beta;
         }
       }
-      p = warp_sum(p);
-      if (lane == 0) s_norm[(j + 1) & 1] = p;
-    }
-    if (threadIdx.x == 0) {
-      s_tau[jj] = h.tau;
-      s_scale[jj] = h.scale;
-      s_beta[jj] = h.beta;
     }
     __syncthreads();
   }
@@ -242,12 +241,16 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
   }
   __syncthreads();
   // finalise: v tails = x * scale, diagonal = beta
-  for (int e = threadIdx.x; e < nbp * (m - j0); e += blockDim.x) {
-    const int q = e / (m - j0), i = j0 + e % (m - j0);
+  const int rows = m - j0;
+  for (int q = 0; q < nbp; ++q) {
     const int c = j0 + q;
-    if (i > c) A[i + c * lda] *= s_scale[c];
-    else if (i == c) A[i + c * lda] = s_beta[c];
+    const double sc = s_scale[c];
+    for (int i = j0 + threadIdx.x; i < m; i += blockDim.x) {
+      if (i > c) A[i + c * lda] *= sc;
+      else if (i == c) A[i + c * lda] = s_beta[c];
+    }
   }
+  (void)rows;
   __syncthreads();
 }
 
@@ -263,20 +266,22 @@ HBS_DEV void form_t(double* T, const double* G, const double* s_tau, int j0, int
   }
 }
 
-// Inverse of R's diagonal block (panel j0), by one warp: lane c solves R x = e_c.
+// Inverse of R's diagonal block (panel j0), by one warp: lane c computes
+// column c of R^{-1} (x = e_c; for i = 31..0: x_i /= R_ii; x_k -= R_ki x_i, k < i).
 HBS_DEV void diag_block_inverse(const double* A, int lda, int j0, int nbp, double* out) {
   const int c = threadIdx.x & 31;
   double x[kP];
 #pragma unroll
-  for (int i = kP - 1; i >= 0; --i) {
-    double acc = (i == c) ? 1.0 : 0.0;
+  for (int i = 0; i < kP; ++i) x[i] = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = i + 1; k < kP; ++k) {
-      const double rik = (i < nbp && k < nbp) ? A[(j0 + i) + (j0 + k) * lda] : 0.0;
-      acc = fma(-rik, x[k], acc);
-    }
+  for (int i = kP - 1; i >= 0; --i) {
     const double rii = (i < nbp) ? A[(j0 + i) + (j0 + i) * lda] : 1.0;
-    x[i] = acc / rii;
+    x[i] = x[i] / rii;
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      const double rki = (i < nbp) ? A[(j0 + k) + (j0 + i) * lda] : 0.0;
+      x[k] = fma(-rki, x[i], x[k]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < kP; ++i) out[i * kP + c] = x[i];
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(512) hqr_kernel(GeqrfArgs args) {
   double* s_scale = s_tau + args.n_max;
   double* s_beta = s_scale + args.n_max;
   double* s_norm = s_beta + args.n_max;
-  double* G = smem + round_up(3 * args.n_max + 2, 2);
+  double* G = smem + round_up(3 * args.n_max + 6, 2);
   double* Tbase = G + kP * kLdT;
   const int tslots = (args.mode == kGeqrfOrtho) ? (args.n_max + kP - 1) / kP : 1;
   double* A = SMEM ? Tbase + (size_t)round_up(kP * kLdT * tslots, 2)
@@ -380,43 +385,55 @@ __global__ void __launch_bounds__(512) hqr_kernel(GeqrfArgs args) {
     const double* T = Tbase + p * kP * kLdT;
     // columns right of the panel already hold Q; apply the block reflector
     if (j0 + kP < n) block_reflector_apply(A, lda, mp8, j0, nbp, T, false, j0 + kP, n);
-    // S = T V1^T (nbp x nbp) -> G, where V1 = V(j0:j0+nbp, :)
-    if (warp == 0) {
-      const int a = threadIdx.x & 31;
-      for (int c = 0; c < kP; ++c) {
-        double acc = 0.0;
-        for (int q = 0; q < kP; ++q) acc = fma(T[a * kLdT + q], vval(A, lda, j0, nbp, j0 + c, q), acc);
-        G[a * kLdT + c] = acc;
-      }
-    }
-    __syncthreads();
-    // panel columns: Q(i, j0+c) = delta(i, j0+c) - sum_q V(i, q) S(q, c), i >= j0; 0 above.
-    // Two passes (compute, sync, write) because V lives in the same columns.
-    const int rows = mp8 - j0;
-    constexpr int kMaxPer = 16;  // values per thread per pass
-    for (int base = 0; base < rows * nbp; base += blockDim.x * kMaxPer) {
-      double vals[kMaxPer];
+    // S = T V1^T (32 x 32) -> G, one 8x8 fragment per warp (V1 = V(j0:j0+32, :))
+    {
+      const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+      if (warp < 16) {
+        const int fi = warp >> 2, fj = warp & 3;
+        double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        const int e = base + threadIdx.x + u * blockDim.x;
-        vals[u] = 0.0;
-        if (e < rows * nbp) {
-          const int c = e / rows, i = j0 + e % rows;
-          double acc = (i == j0 + c) ? 1.0 : 0.0;
-          for (int q = 0; q < nbp; ++q) acc = fma(-vval(A, lda, j0, nbp, i, q), G[q * kLdT + c], acc);
-          vals[u] = acc;
+        for (int kk = 0; kk < kP; kk += 4) {
+          const double av = T[(8 * fi + g) * kLdT + kk + t];
+          const double bv = vval(A, lda, j0, nbp, j0 + 8 * fj + g, kk + t);   // V1^T(q, c) = V(j0 + c, q)
+          dmma8x8x4(c0, c1, av, bv);
+        }
+        G[(8 * fi + g) * kLdT + 8 * fj + 2 * t] = c0;
+        G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + 1] = c1;
+      }
+      __syncthreads();
+      // Q panel rows j0.. in 8-row blocks: Q = E - V_p S (computed, then written after a barrier)
+      const int nrb = (mp8 - j0) >> 3;
+      double qv[4][4][2];   // up to 4 row blocks per warp
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rbk = warp + u * (blockDim.x >> 5);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) { qv[u][f][0] = 0.0; qv[u][f][1] = 0.0; }
+        if (rbk < nrb) {
+          const int i = j0 + 8 * rbk + g;
+#pragma unroll
+          for (int kk = 0; kk < kP; kk += 4) {
+            const double av = -vval(A, lda, j0, nbp, i, kk + t);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) dmma8x8x4(qv[u][f][0], qv[u][f][1], av, G[(kk + t) * kLdT + 8 * f + g]);
+          }
         }
       }
       __syncthreads();
 #pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        const int e = base + threadIdx.x + u * blockDim.x;
-        if (e < rows * nbp) {
-          const int c = e / rows, i = j0 + e % rows;
-          A[i + (j0 + c) * lda] = vals[u];
+      for (int u = 0; u < 4; ++u) {
+        const int rbk = warp + u * (blockDim.x >> 5);
+        if (rbk < nrb) {
+          const int i = j0 + 8 * rbk + g;
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = 8 * f + 2 * t + e;
+              if (c < nbp) A[i + (j0 + c) * lda] = qv[u][f][e] + (i == j0 + c ? 1.0 : 0.0);
+            }
         }
       }
-      __syncthreads();
     }
     for (int e = threadIdx.x; e < j0 * nbp; e += blockDim.x) {
       const int c = e / j0, i = e % j0;
@@ -434,7 +451,7 @@ __global__ void __launch_bounds__(512) hqr_kernel(GeqrfArgs args) {
 size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix) {
   const int lda = frag_ld(round_up(m_max, 32));
   const int np = (mode == kGeqrfOrtho) ? (n_max + kP - 1) / kP : 1;
-  size_t d = round_up(3 * n_max + 2, 2) + kP * kLdT + round_up(kP * kLdT * np, 2);
+  size_t d = round_up(3 * n_max + 6, 2) + kP * kLdT + round_up(kP * kLdT * np, 2);
   if (with_matrix) d += (size_t)lda * n_max;
   return d * sizeof(double);
 }

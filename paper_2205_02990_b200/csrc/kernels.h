@@ -102,6 +102,8 @@ struct ApplyQArgs {
   int n_fixed, n_is_rows, n_max;
 };
 int launch_applyq(ApplyQArgs args, int nsides, cudaStream_t stream);
+size_t applyq2_smem_bytes(int s);
+int launch_applyq2(ApplyQArgs args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- batched GEMM
 // Operand addressing for box b: base + c_rb*row_begin[b] + c_b*b + c_sq*sq_off[b];
