@@ -4,7 +4,10 @@ reference's golden fixtures.
 Parity contract:
   * oversampled twins (r > k): ||(A_gpu - A_ref) x|| / ||A_ref x|| <= 1e-10;
   * literal configs (r = k, rounding-chaotic in the reference itself):
-    ||(A_gpu - A) x|| / ||A x|| <= 10 x the reference's own error vs the truth;
+    ||(A_gpu - A) x|| / ||A x|| <= 10 x the reference's own error vs the truth,
+    where "the reference's own error" is the max over the reference run on the
+    exact samples and on six 1e-16-relative perturbations of (Y, Z) (recorded
+    in the golden fixture by oracle/make_golden.py with the real reference);
   * node-level: projectors U U^T, V V^T and D of the first leaf / level-1 node
     within 1e-10 of the reference when the case is well conditioned.
 """
@@ -45,7 +48,7 @@ def test_golden_operator_parity(name):
     f = gpu_compress(c["samples"], c["n"], c["leaf"], c["r"])
     ax = hb.apply_matrix(f, c["x"])
     atx = hb.apply_matrix(f, c["x"], transpose=True)
-    ref_err = float(g["ref_err_vs_truth"])
+    ref_err = max([float(g["ref_err_vs_truth"])] + [float(v) for v in g["ref_err_perturbed"]])
     err_truth = rel(ax, g["true_ax"])
     if c["literal"]:
         assert err_truth <= 10.0 * ref_err, (err_truth, ref_err)
