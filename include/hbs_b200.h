@@ -89,6 +89,22 @@ int hbs_compress_level_profiled(int64_t nbox, const int64_t* row_begin, const in
                                 void* workspace, size_t workspace_bytes, int32_t* status, void* stream,
                                 float* phase_ms);
 
+/* Building block: batched Householder QR of Omega_tau^T for every box of a
+ * level -- the factorisation numpy.linalg.qr(mode="complete") performs inside
+ * the reference's nullspace() (linalg.py:52-62), with LAPACK's dlarfg
+ * reflector convention.  Per box b (uniform strides by max_rows = nr):
+ *   vt   : nr x s, reflector j as row j (unit diagonal, zeros before it)
+ *   r    : nr x nr upper triangular R  (Omega_tau^T = Q R)
+ *   tau  : nr reflector scalars
+ *   t    : ceil(nr/32) compact-WY T blocks (32 x 32, row-major)
+ *   rinv : ceil(nr/32) inverses of R's 32 x 32 diagonal blocks
+ *   status[b] = 1 when min|R_ii| < tol max|R_ii| (rank-deficient probe block)
+ * scratch: hbs_probe_qr_scratch_bytes (0 unless a matrix exceeds shared memory). */
+int hbs_probe_qr_scratch_bytes(int64_t nbox, int max_rows, int s, size_t* bytes);
+int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int s,
+                 double tol, const double* omega, double* vt, double* r, double* tau, double* t, double* rinv,
+                 double* scratch, int32_t* status, void* stream);
+
 /* Number of CUDA kernels launched by this library so far (process-wide). */
 unsigned long long hbs_launch_counter(void);
 

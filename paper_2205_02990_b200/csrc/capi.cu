@@ -275,6 +275,35 @@ int hbs_compress_level_profiled(int64_t nbox, const int64_t* row_begin, const in
   return rc;
 }
 
+int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int s,
+                 double tol, const double* omega, double* vt, double* r, double* tau, double* t, double* rinv,
+                 double* scratch, int32_t* status, void* stream) {
+  if (nbox < 1 || max_rows < 1 || s < max_rows) return HBS_ERR_DIMENSION;
+  if (s > 512) return HBS_ERR_UNSUPPORTED;
+  const LevelGeo geo{row_begin, sq_off, nbox};
+  const int nr = max_rows, npanel = (nr + kNB - 1) / kNB;
+  GeqrfArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = geo; g.mode = kGeqrfFactor;
+  g.m_fixed = s; g.m_is_rows = 0; g.n_fixed = 0; g.n_is_rows = 1;
+  g.m_max = s; g.n_max = nr; g.tol = tol; g.gscratch = scratch;
+  GeqrfSide& S = g.side[0];
+  S.src = omega; S.src_c_rb = s; S.src_c_b = 0; S.src_rs = 1; S.src_cs = s;
+  S.vt = vt; S.vt_stride = (int64_t)nr * s; S.ldvt = s;
+  S.r = r; S.r_stride = (int64_t)nr * nr; S.ldr = nr;
+  S.tau = tau; S.tau_stride = nr;
+  S.t = t; S.t_stride = (int64_t)npanel * kNB * kNB;
+  S.rinv = rinv; S.rinv_stride = (int64_t)npanel * kNB * kNB;
+  S.status = status;
+  return launch_hqr(g, 1, static_cast<cudaStream_t>(stream));
+}
+
+int hbs_probe_qr_scratch_bytes(int64_t nbox, int max_rows, int s, size_t* bytes) {
+  if (!bytes) return HBS_ERR_DIMENSION;
+  *bytes = hqr_fits_smem(s, max_rows, kGeqrfFactor) ? 0 : hqr_scratch_doubles(s, max_rows, nbox) * sizeof(double);
+  return HBS_OK;
+}
+
 int hbs_root_workspace_bytes(int rows, int s, size_t* bytes) {
   if (rows < 1 || s < 1 || !bytes) return HBS_ERR_DIMENSION;
   Carver c{nullptr};

@@ -151,7 +151,8 @@ template <int MR, int CPW>
 HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
                           double* s_beta, double* s_norm) {
   // Warp w owns panel columns j0 + w + nw*u (u < CPW), rows j0 + lane + 32k in x[u][k].
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int nw = 32 / CPW;        // warps per CTA (compile time)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
   double x[CPW][MR];
   int clast = -1;
@@ -196,7 +197,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
       }
       // which of my columns is the next pivot (its norm is folded into the same reduction)
       const int nxt = jj + 1;
-      const int unx = (nxt - j0 - warp) % nw == 0 && nxt - j0 - warp >= 0 && j + 1 < nbp ? (nxt - j0 - warp) / nw : -1;
+      const int unx = (j + 1 < nbp && ((j + 1) & (nw - 1)) == warp) ? (j + 1) / nw : -1;
       double d[CPW], r_[CPW];
 #pragma unroll
       for (int u = 0; u < CPW; ++u) {

@@ -1,0 +1,96 @@
+"""GPU kernel-level parity through the C-ABI building blocks: the batched
+Householder QR (reference: numpy.linalg.qr / LAPACK dgeqrf, as called by
+nullspace(), linalg.py:52-62)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2205_02990_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _native.lib()
+
+
+def probe_qr(blocks, s):
+    """Run hbs_probe_qr on a list of (rows x s) probe blocks (uneven sizes allowed)."""
+    rows = [b.shape[0] for b in blocks]
+    nr = max(rows)
+    begins = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    sq = np.concatenate([[0], np.cumsum(np.array(rows) ** 2)]).astype(np.int64)
+    nbox = len(blocks)
+    dev = torch.device("cuda")
+    om = torch.from_numpy(np.concatenate(blocks)).to(dev)
+    rb, so = torch.from_numpy(begins).to(dev), torch.from_numpy(sq).to(dev)
+    npan = (nr + 31) // 32
+    vt = torch.zeros(nbox, nr, s, dtype=torch.float64, device=dev)
+    r = torch.zeros(nbox, nr, nr, dtype=torch.float64, device=dev)
+    tau = torch.zeros(nbox, nr, dtype=torch.float64, device=dev)
+    t = torch.zeros(nbox, npan, 32, 32, dtype=torch.float64, device=dev)
+    rinv = torch.zeros(nbox, npan, 32, 32, dtype=torch.float64, device=dev)
+    st = torch.zeros(nbox, dtype=torch.int32, device=dev)
+    sz = ctypes.c_size_t()
+    _native.check(_native.lib().hbs_probe_qr_scratch_bytes(nbox, nr, s, ctypes.byref(sz)), "scratch")
+    scratch = torch.empty(max(sz.value // 8, 1), dtype=torch.float64, device=dev)
+    rc = _native.lib().hbs_probe_qr(nbox, rb.data_ptr(), so.data_ptr(), nr, s, 1e-10, om.data_ptr(), vt.data_ptr(),
+                                    r.data_ptr(), tau.data_ptr(), t.data_ptr(), rinv.data_ptr(),
+                                    scratch.data_ptr() if sz.value else 0, st.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream)
+    _native.check(rc, "hbs_probe_qr")
+    torch.cuda.synchronize()
+    return [x.cpu().numpy() for x in (vt, r, tau, t, rinv, st)]
+
+
+@pytest.mark.parametrize("rows,s", [(128, 192), (64, 96), (32, 48), (40, 120), (144, 216), (21, 45), (7, 30)])
+def test_probe_qr_matches_lapack(rows, s):
+    rng = np.random.default_rng(rows * 1000 + s)
+    blocks = [rng.standard_normal((rows, s)) for _ in range(5)]
+    vt, r, tau, t, rinv, st = probe_qr(blocks, s)
+    assert not st.any()
+    for b, om in enumerate(blocks):
+        n = om.shape[0]
+        # LAPACK (numpy) complete QR of omega^T: same reflectors => same R and Q
+        q_ref, r_ref = np.linalg.qr(om.T, mode="complete")
+        R = r[b][:n, :n]
+        assert np.abs(R - r_ref[:n, :n]).max() <= 1e-12 * np.abs(r_ref).max()
+        q = np.eye(s)
+        for j in range(n - 1, -1, -1):
+            v = vt[b][j]
+            q -= tau[b][j] * np.outer(v, v @ q)
+        assert np.abs(q - q_ref).max() <= 1e-12
+        assert np.linalg.norm(q.T @ q - np.eye(s)) <= 1e-13 * s
+        # the trailing ("last r columns") null basis equals the reference's nullspace()
+        assert np.abs(om @ q[:, n:]).max() <= 1e-12 * np.abs(om).max()
+        # compact-WY T blocks and diagonal-block inverses
+        for p in range((n + 31) // 32):
+            j0, nbp = 32 * p, min(32, n - 32 * p)
+            V = vt[b][j0:j0 + nbp].T
+            Hblk = np.eye(s) - V @ t[b][p][:nbp, :nbp] @ V.T
+            Hseq = np.eye(s)
+            for j in range(j0, j0 + nbp):
+                Hseq = Hseq @ (np.eye(s) - tau[b][j] * np.outer(vt[b][j], vt[b][j]))
+            assert np.abs(Hblk - Hseq).max() <= 1e-13
+            Rb = R[j0:j0 + nbp, j0:j0 + nbp]
+            assert np.abs(rinv[b][p][:nbp, :nbp] @ Rb - np.eye(nbp)).max() <= 1e-12
+
+
+def test_probe_qr_flags_rank_deficiency():
+    rng = np.random.default_rng(5)
+    om = rng.standard_normal((16, 40))
+    om[3] = om[0]
+    ok = rng.standard_normal((16, 40))
+    *_, st = probe_qr([ok, om, ok], 40)
+    assert list(st) == [0, 1, 0]
+
+
+def test_probe_qr_zero_block():
+    vt, r, tau, t, rinv, st = probe_qr([np.zeros((8, 20))], 20)
+    assert st[0] == 1          # sigma_max == 0 -> rank deficient (linalg.py:73)
+    assert not np.any(tau)     # dlarfg: zero column -> tau = 0, H = I
