@@ -61,6 +61,8 @@ def lib():
         except OSError as exc:
             raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
         for name, (args, res) in SIGNATURES.items():
+            if not hasattr(handle, name):
+                raise NativeError(f"{LIB_PATH} does not export {name}")
             fn = getattr(handle, name)
             fn.argtypes = args
             fn.restype = res

@@ -64,6 +64,23 @@ inline __host__ __device__ int frag_ld(int cols) {
 
 inline __host__ __device__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// mbarrier helpers (shared::cta).
+HBS_DEV void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+HBS_DEV void mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(a) : "memory");
+}
+HBS_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+
 // cp.async (LDGSTS) helpers: 8-byte element copies with zero fill.
 HBS_DEV void cp_async8(double* dst, const double* src, bool pred) {
   const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));

@@ -22,6 +22,16 @@
 
 namespace hbs {
 
+#ifdef HBS_TRACE
+__device__ long long g_hqr_trace[256];
+__device__ int g_hqr_trace_mode = 0;   // record only kernels of this mode
+#define HQR_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && args.mode == g_hqr_trace_mode) g_hqr_trace[i] = clock64(); } while (0)
+#define HQR_STEP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0) g_hqr_trace[64 + (i)] = clock64(); } while (0)
+#else
+#define HQR_MARK(i) do { } while (0)
+#define HQR_STEP(i) do { } while (0)
+#endif
+
 namespace {
 
 constexpr int kP = 32;        // panel width (== kNB)
@@ -32,11 +42,17 @@ struct Reflector {  // dlarfg for the current pivot
 };
 
 HBS_DEV Reflector make_reflector(double alpha, double xn2) {
+  // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta,
+  // x <- x / (alpha - beta).  Division-free form: with rho = 1 / ||(alpha, x)||,
+  // tau = 1 + |alpha| rho and 1 / (alpha - beta) = sign(alpha) / (|alpha| + ||.||).
   Reflector h{0.0, alpha, 0.0};
-  if (xn2 != 0.0) {  // beta = -sign(alpha) * hypot(alpha, ||x||)
-    h.beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-    h.tau = (h.beta - alpha) / h.beta;
-    h.scale = 1.0 / (alpha - h.beta);
+  if (xn2 != 0.0) {
+    const double s2 = fma(alpha, alpha, xn2);
+    const double rho = rsqrt(s2);
+    const double nrm = s2 * rho;
+    h.beta = -copysign(nrm, alpha);
+    h.tau = fma(fabs(alpha), rho, 1.0);
+    h.scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
   }
   return h;
 }
@@ -147,124 +163,213 @@ HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp
 // Factor panel j0 (nbp <= 32 columns) in place.  Leaves: pre-scale reflector
 // values in A (finalised afterwards by the caller), tau/scale/beta in smem,
 // G(c, j) = v_c . v_j (c < j) in G.
-template <int MR, int CPW>
+// Panel factorisation in 8-column sub-panels.  In sub-panel q, warp w < 8 owns
+// column cs + w (cs = j0 + 8q) in registers (rows j0 + lane + 32k).  Step j
+// needs only pivot j: its owner publishes (column in A, tau/scale/beta in
+// smem) and arrives on bar[j]; the others wait on bar[j] alone.  bar[] completes
+// once per panel (parity = panel & 1).  The owners of earlier sub-panel columns
+// form the compact-WY dots v_c . v_j on the fly (G8); after the 8 steps the
+// sub-panel's block reflector is applied to the rest of the panel on the
+// tensor cores, so only 8 warps ever contend for issue during a step.
+template <int MR>
 HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
-                          double* s_beta, double* s_norm) {
-  // Warp w owns panel columns j0 + w + nw*u (u < CPW), rows j0 + lane + 32k in x[u][k].
-  constexpr int nw = 32 / CPW;        // warps per CTA (compile time)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                          double* s_beta, uint64_t* bar, unsigned parity, double* G8, double* T8,
+                          double* wpart, double* wfin) {
+  constexpr int kSub = 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
   const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
-  double x[CPW][MR];
-  int clast = -1;
+  for (int cs = j0; cs < j0 + nbp; cs += kSub) {
+    const int nsub = min(kSub, j0 + nbp - cs);
+    const int jq = cs - j0;           // step index of the sub-panel's first pivot
+    if (warp < nsub) {
+      const int c = cs + warp;
+      double x[MR];
 #pragma unroll
-  for (int u = 0; u < CPW; ++u) {
-    const int c = j0 + warp + nw * u;
-    const bool own = (c - j0) < nbp;
-    if (own) clast = c;
+      for (int k = 0; k < MR; ++k) x[k] = (k < kc) ? A[(j0 + lane + 32 * k) + c * lda] : 0.0;
+      if (warp == 0) {  // first pivot of the sub-panel: exact norm
+        double p = 0.0;
 #pragma unroll
-    for (int k = 0; k < MR; ++k) x[u][k] = (own && k < kc) ? A[(j0 + lane + 32 * k) + c * lda] : 0.0;
-  }
-  if (warp == 0) {  // reflector of the first pivot (column j0 is warp 0, slot u = 0)
-    double p = 0.0;
-#pragma unroll
-    for (int k = 0; k < MR; ++k) {
-      const int row = j0 + lane + 32 * k;
-      if (k < kc && row > j0) p = fma(x[0][k], x[0][k], p);
-    }
-    p = warp_sum(p);
-    const double alpha = __shfl_sync(0xffffffffu, x[0][0], 0);
-    if (lane == 0) {
-      const Reflector h = make_reflector(alpha, p);
-      s_norm[0] = h.tau; s_norm[1] = h.scale; s_norm[2] = h.beta;
-    }
-  }
-  __syncthreads();
-  for (int j = 0; j < nbp; ++j) {
-    const int jj = j0 + j;
-    const double* sn = s_norm + 3 * (j & 1);
-    const double tau = sn[0], scale = sn[1];
-    if (threadIdx.x == 0) {
-      s_tau[jj] = tau;
-      s_scale[jj] = scale;
-      s_beta[jj] = sn[2];
-    }
-    if (clast > jj) {
-      double pv[MR];
-#pragma unroll
-      for (int k = 0; k < MR; ++k) {
-        const int row = j0 + lane + 32 * k;
-        pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+        for (int k = 0; k < MR; ++k) {
+          const int row = j0 + lane + 32 * k;
+          if (k < kc && row > cs) p = fma(x[k], x[k], p);
+        }
+        p = warp_sum(p);
+        const double alpha = __shfl_sync(0xffffffffu, x[0], jq);   // row cs: slot 0, lane jq (< 32)
+        if (lane == 0) {
+          const Reflector h = make_reflector(alpha, p);
+          s_tau[cs] = h.tau; s_scale[cs] = h.scale; s_beta[cs] = h.beta;
+          mbar_arrive(&bar[jq]);
+          HQR_STEP(jq);
+        }
       }
-      // which of my columns is the next pivot (its norm is folded into the same reduction)
-      const int nxt = jj + 1;
-      const int unx = (j + 1 < nbp && ((j + 1) & (nw - 1)) == warp) ? (j + 1) / nw : -1;
-      double d[CPW], r_[CPW];
+      for (int i = 0; i < nsub; ++i) {
+        const int jj = cs + i, j = jq + i;
+        if (c == jj) continue;
+        mbar_wait(&bar[j], parity);
+        const double tau = s_tau[jj], scale = s_scale[jj];
+        double pv[MR];
 #pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        r_[u] = __shfl_sync(0xffffffffu, x[u][0], j);  // row jj sits in slot 0 of lane j
-        double a = 0.0;
+        for (int k = 0; k < MR; ++k) {
+          const int row = j0 + lane + 32 * k;
+          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+        }
+        const bool pub = (c == jj + 1);   // I publish the next pivot
+        double d = 0.0, sxx = 0.0, spp = 0.0;
 #pragma unroll
-        for (int k = 0; k < MR; ++k) a = fma(pv[k], x[u][k], a);
-        d[u] = a;
-      }
+        for (int k = 0; k < MR; ++k) {
+          d = fma(pv[k], x[k], d);
+          if (pub) {
+            const int row = j0 + lane + 32 * k;
+            if (row > jj + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
+          }
+        }
+        const double rj = __shfl_sync(0xffffffffu, x[0], j);   // my value in row jj (slot 0, lane j < 32)
+        double xn_old = 0.0, pn = 0.0;
+        if (pub) {
+          pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+          xn_old = __shfl_sync(0xffffffffu, x[0], j + 1);
+        }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 16; o > 0; o >>= 1) {
+          d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (pub) {
+            sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+            spp += __shfl_xor_sync(0xffffffffu, spp, o);
+          }
+        }
+        if (c < jj) {   // compact-WY dot v_c . v_jj (my column is a retired reflector)
+          if (lane == 0) G8[(c - cs) * kSub + i] = s_scale[c] * (rj + scale * d);
+          continue;
+        }
+        const double f = tau * (rj + scale * d), gs = f * scale;
 #pragma unroll
-        for (int u = 0; u < CPW; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
-      }
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        const int c = j0 + warp + nw * u;
-        if (c > jj && (c - j0) < nbp) {
-          const double f = tau * (r_[u] + scale * d[u]), gs = f * scale;
-#pragma unroll
-          for (int k = 0; k < MR; ++k) x[u][k] = fma(-gs, pv[k], x[u][k]);
-          if (lane == j) x[u][0] -= f;
-          if (u == unx) {
+        for (int k = 0; k < MR; ++k) x[k] = fma(-gs, pv[k], x[k]);
+        if (lane == j) x[0] -= f;
+        if (pub) {
+          const double sxp = d - pn * xn_old;
+          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
+          if (!(nrm > 0.5 * sxx)) {   // cancellation: recompute exactly
             double p = 0.0;
 #pragma unroll
             for (int k = 0; k < MR; ++k) {
               const int row = j0 + lane + 32 * k;
-              if (k < kc && row > nxt) p = fma(x[u][k], x[u][k], p);
+              if (k < kc && row > jj + 1) p = fma(x[k], x[k], p);
             }
-            const double nrm = warp_sum(p);
-            // publish the next pivot: column, reflector
+            nrm = warp_sum(p);
+          }
 #pragma unroll
-            for (int k = 0; k < MR; ++k)
-              if (k < kc) A[(j0 + lane + 32 * k) + nxt * lda] = x[u][k];
-            const double alpha = __shfl_sync(0xffffffffu, x[u][0], j + 1);
-            if (lane == 0) {
-              const Reflector h = make_reflector(alpha, nrm);
-              double* so = s_norm + 3 * ((j + 1) & 1);
-              so[0] = h.tau; so[1] = h.scale; so[2] = h.beta;
-            }
+          for (int k = 0; k < MR; ++k)
+            if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
+          const double alpha = __shfl_sync(0xffffffffu, x[0], j + 1);
+          __syncwarp();
+          if (lane == 0) {
+            const Reflector h = make_reflector(alpha, nrm);
+            s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+            mbar_arrive(&bar[j + 1]);
+            HQR_STEP(j + 1);
           }
         }
       }
-    }
-    __syncthreads();
-  }
-  // write back the owned columns (final values, reflector tails unscaled)
-#pragma unroll
-  for (int u = 0; u < CPW; ++u) {
-    const int c = j0 + warp + nw * u;
-    if ((c - j0) < nbp) {
 #pragma unroll
       for (int k = 0; k < MR; ++k)
-        if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[u][k];
+        if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
     }
-  }
-  __syncthreads();
-  // finalise: v tails = x * scale, diagonal = beta
-  for (int q = 0; q < nbp; ++q) {
-    const int c = j0 + q;
-    const double sc = s_scale[c];
-    for (int i = j0 + threadIdx.x; i < m; i += blockDim.x) {
-      if (i > c) A[i + c * lda] *= sc;
-      else if (i == c) A[i + c * lda] = s_beta[c];
+    __syncthreads();
+    if (threadIdx.x == 0) HQR_STEP(40 + (jq >> 3) * 4);
+    // finalise the sub-panel: v tails = x * scale, diagonal = beta
+    for (int q = 0; q < nsub; ++q) {
+      const int c = cs + q;
+      const double sc = s_scale[c];
+      for (int i = c + threadIdx.x; i < m; i += blockDim.x) {
+        if (i > c) A[i + c * lda] *= sc;
+        else A[i + c * lda] = s_beta[c];
+      }
     }
+    const int c1 = cs + kSub, c2 = j0 + nbp;   // remaining panel columns
+    if (c1 < c2) {
+      // T8 (dlarft recurrence, lanes 0..7 of warp 0); meanwhile warps 1..4
+      // form partial W = V_sub^T X_rest over K chunks.
+      if (warp == 0) {
+        if (lane < kSub) {
+          double trow[kSub];
+#pragma unroll
+          for (int cc = 0; cc < kSub; ++cc) {
+            const double tc = (cc < nsub) ? s_tau[cs + cc] : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < cc; ++q)
+              if (q >= lane) acc = fma(trow[q], G8[q * kSub + cc], acc);
+            trow[cc] = (lane < cc) ? -tc * acc : (lane == cc ? tc : 0.0);
+          }
+#pragma unroll
+          for (int cc = 0; cc < kSub; ++cc) T8[lane * kSub + cc] = trow[cc];
+        }
+      }
+      __syncthreads();   // finalised V visible
+      if (threadIdx.x == 0) HQR_STEP(41 + (jq >> 3) * 4);
+      const int kspan = round_up(m - cs, 4);
+      const int nsplit = 4;
+      const int kchunk = round_up((kspan + nsplit - 1) / nsplit, 4);
+      if (warp >= 1 && warp <= nsplit) {
+        const int ws = warp - 1;
+        const int kb = cs + ws * kchunk, ke = min(cs + kspan, kb + kchunk);
+        double w[3][2] = {};
+        for (int k = kb; k < ke; k += 4) {
+          const int i = k + t;
+          // A = V_sub^T (row g = reflector, col = row index i)
+          const double av = (g < nsub && i >= cs + g) ? (i == cs + g ? 1.0 : A[i + (cs + g) * lda]) : 0.0;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const int cc = c1 + 8 * f + g;
+            const double bv = cc < c2 ? A[i + cc * lda] : 0.0;
+            dmma8x8x4(w[f][0], w[f][1], av, bv);
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          wpart[ws * 192 + g * 24 + 8 * f + 2 * t] = w[f][0];
+          wpart[ws * 192 + g * 24 + 8 * f + 2 * t + 1] = w[f][1];
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) HQR_STEP(42 + (jq >> 3) * 4);
+      // W' = T8^T (sum of partials)  (8 x 24)
+      for (int e = threadIdx.x; e < 192; e += blockDim.x) {
+        const int q = e / 24, cc = e % 24;
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < kSub; ++a) {
+          const double wa = wpart[a * 24 + cc] + wpart[192 + a * 24 + cc] + wpart[384 + a * 24 + cc] +
+                            wpart[576 + a * 24 + cc];
+          acc = fma(T8[a * kSub + q], wa, acc);
+        }
+        wfin[e] = acc;
+      }
+      __syncthreads();
+      // X_rest(rows cs.., c1..c2) -= V_sub W'
+      const int nrb = (round_up(m, 8) - cs + 7) >> 3;
+      for (int u = warp; u < nrb * 3; u += nw) {
+        const int rbk = u / 3, f = u % 3;
+        const int i = cs + 8 * rbk + g;
+        const int col = c1 + 8 * f + 2 * t;
+        if (c1 + 8 * f >= c2) continue;
+        double c0v = (col < c2) ? A[i + col * lda] : 0.0;
+        double c1v = (col + 1 < c2) ? A[i + (col + 1) * lda] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kSub; kk += 4) {
+          const int q = kk + t;
+          const double av = (q < nsub && i >= cs + q) ? (i == cs + q ? 1.0 : A[i + (cs + q) * lda]) : 0.0;
+          const double bv = -wfin[q * 24 + 8 * f + g];
+          dmma8x8x4(c0v, c1v, av, bv);
+        }
+        if (col < c2) A[i + col * lda] = c0v;
+        if (col + 1 < c2) A[i + (col + 1) * lda] = c1v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) HQR_STEP(43 + (jq >> 3) * 4);
   }
-  __syncthreads();
 }
 
 // G = V_p^T V_p (32 x 32) on the tensor cores; warp w < 16 computes one 8x8 block.
@@ -397,14 +502,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
   double* s_tau = smem;
   double* s_scale = s_tau + args.n_max;
   double* s_beta = s_scale + args.n_max;
-  double* s_norm = s_beta + args.n_max;
-  double* G = smem + round_up(3 * args.n_max + 6, 2);
-  double* Tscr = G + kP * kLdT;     // 256-double scratch for form_t
-  double* Tbase = Tscr + 256;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + args.n_max);   // 32 step barriers
+  double* G = smem + round_up(3 * args.n_max + 32, 2);
+  double* Tscr = G + kP * kLdT;     // 384-double scratch (form_t, sub-panel G8/T8/W')
+  double* Tbase = Tscr + 384;
   const int tslots = (args.mode == kGeqrfOrtho) ? (args.n_max + kP - 1) / kP : 1;
   double* A = SMEM ? Tbase + (size_t)round_up(kP * kLdT * tslots, 2)
                    : args.gscratch + ((size_t)side * args.geo.nbox + b) * (size_t)lda * args.n_max;
 
+  HQR_MARK(0);
   // load, zero-padding rows m .. mpad-1
   const double* src = S.src + S.src_c_rb * rb + S.src_c_b * b;
   if (S.src_rs == 1) {
@@ -424,10 +530,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
   __syncthreads();
 
   const int warp = threadIdx.x >> 5;
+  HQR_MARK(1);
+  if (threadIdx.x < kP) mbar_init(&s_bar[threadIdx.x], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
   for (int p = 0; p < npanel; ++p) {
     const int j0 = p * kP, nbp = min(kP, n - j0);
     double* T = Tbase + (args.mode == kGeqrfOrtho ? p * kP * kLdT : 0);
-    panel_factor<MR, CPW>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_norm);
+    HQR_MARK(2 + 4 * p);
+    panel_factor<MR>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr, Tscr + 64, G,
+                     Tscr + 128);
+    HQR_MARK(3 + 4 * p);
     panel_gram(A, lda, m, j0, nbp, G);
     __syncthreads();
     form_t(T, Tscr, G, s_tau, j0, nbp);
@@ -435,10 +548,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
       double* tout = S.t + (size_t)b * S.t_stride + (size_t)p * kP * kP;
       for (int e = threadIdx.x; e < kP * kP; e += blockDim.x) tout[e] = T[(e / kP) * kLdT + e % kP];
     }
+    HQR_MARK(4 + 4 * p);
     if (j0 + kP < n) block_reflector_apply(A, lda, round_up(m, 8), j0, nbp, T, true, j0 + kP, n);
+    HQR_MARK(5 + 4 * p);
     __syncthreads();
   }
 
+  HQR_MARK(40);
   if (args.mode == kGeqrfFactor) {
     if (threadIdx.x < 32) {  // sigma screen on diag(R)
       double lo = INFINITY, hi = 0.0;
@@ -466,6 +582,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
     }
     double* tau = S.tau + (size_t)b * S.tau_stride;
     for (int j = threadIdx.x; j < n; j += blockDim.x) tau[j] = s_tau[j];
+    HQR_MARK(41);
     return;
   }
 
@@ -546,7 +663,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
 size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix) {
   const int lda = frag_ld(round_up(m_max, 32));
   const int np = (mode == kGeqrfOrtho) ? (n_max + kP - 1) / kP : 1;
-  size_t d = round_up(3 * n_max + 6, 2) + kP * kLdT + 256 + round_up(kP * kLdT * np, 2);
+  size_t d = round_up(3 * n_max + 32, 2) + kP * kLdT + 384 + round_up(kP * kLdT * np, 2);
   if (with_matrix) d += (size_t)lda * n_max;
   return d * sizeof(double);
 }
@@ -588,6 +705,15 @@ static int launch_hqr_mr(GeqrfArgs& args, int nsides, cudaStream_t stream) {
   rinv_blocks_kernel<<<grid, 32, 0, stream>>>(args);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+extern "C" int hbs_debug_hqr_trace(long long* out) {
+#ifdef HBS_TRACE
+  return cudaMemcpyFromSymbol(out, g_hqr_trace, sizeof(long long) * 256) == cudaSuccess ? 0 : 4;
+#else
+  (void)out;
+  return 6;
+#endif
 }
 
 int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream) {

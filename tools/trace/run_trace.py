@@ -1,0 +1,37 @@
+"""Run one c4-shaped level with the tracing library and print hqr phase cycles (CTA 0)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", ".."))
+import paper_2205_02990_b200._native as nat
+nat.LIB_PATH = os.path.join(os.path.dirname(__file__), "_hbs_b200_trace.so")
+import torch
+import paper_2205_02990_b200 as hb
+from paper_2205_02990_b200 import synthetic
+tree = hb.build_tree(1 << 14, 128)
+gen = synthetic.device_generator(tree, 64, seed=0, decay=0.9)
+om, ps, y, z = synthetic.device_samples(gen, 192)
+plan = hb.CompressPlan(tree, 192, 64)
+plan.run(om, ps, y, z); torch.cuda.synchronize()
+# single level call for a clean trace of the leaf-level factor kernel
+lib = nat.lib()
+g = plan.geometry[tree.depth]
+u, v, d = plan.levels[tree.depth]
+out = plan.lift[0]
+lib.hbs_compress_level(g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.max_rows, 192, 64, 1e-10,
+                       om.data_ptr(), ps.data_ptr(), y.data_ptr(), z.data_ptr(), u.data_ptr(), v.data_ptr(), d.data_ptr(),
+                       *(m.data_ptr() for m in out), plan.workspace.data_ptr(), plan.workspace_bytes,
+                       plan.status.data_ptr(), 0)
+torch.cuda.synchronize()
+buf = (ctypes.c_longlong * 256)()
+getattr(lib, "hbs_debug_hqr_trace")(buf)
+t = list(buf)
+print("load", t[1] - t[0])
+for p in range(4):
+    a = 2 + 4 * p
+    print(f"panel {p}: factor {t[a+1]-t[a]}  gram+T {t[a+2]-t[a+1]}  trailing {t[a+3]-t[a+2]}")
+print("outputs", t[41] - t[40], "total", t[41] - t[0])
+st = t[64:64 + 32]
+print("step intervals (panel 0):", [st[i + 1] - st[i] for i in range(31)])
+sp = t[64 + 40: 64 + 56]
+for q in range(4):
+    a = sp[4 * q: 4 * q + 4]
+    print(f"sub {q}: end-of-steps->finalised {a[1]-a[0]}  W partial {a[2]-a[1]}  W'+update {a[3]-a[2]}  (steps start {st[8*q]-t[2]})")
