@@ -107,49 +107,69 @@ def _size_t():
     return ctypes.c_size_t()
 
 
-class CompressPlan:
-    """Buffers + launch sequence of one (tree, s, r) compression on one device.
+def tree_level_specs(tree: ClusterTree, rank: int, top_level: int = 1):
+    """(level, row starts, first box index) for levels L .. top_level of a whole tree."""
+    specs = []
+    for level in range(tree.depth, top_level - 1, -1):
+        if level == tree.depth:
+            begins = tree.level_begin(level)
+        else:
+            begins = np.arange((1 << level) + 1, dtype=np.int64) * 2 * rank
+        specs.append((level, begins, 0))
+    return specs
 
-    Everything is allocated up front, so `run()` only enqueues kernels on a
-    stream: it can be timed with CUDA events or captured in a CUDA graph."""
+
+class CompressPlan:
+    """Buffers + launch sequence of a level sweep on one device.
+
+    `specs` lists the levels to compress, deepest first, as (level, row starts
+    of the level's boxes, index of the first box within the global level);
+    the default is the whole tree of `tree`.  With `with_root` the root core
+    is solved after the last (level-1) sweep.  Everything is allocated up
+    front, so `run()` only enqueues kernels on a stream: it can be timed with
+    CUDA events or captured in a CUDA graph.  After `run`, `top_quad` holds
+    the lifted quadruple of the last compressed level (the multi-GPU hand-off)."""
 
     def __init__(self, tree: ClusterTree, s: int, rank: int, tol: float = DEFAULT_ILL_CONDITIONING_TOL,
-                 device=None, top_level: int = 1):
+                 device=None, specs=None, with_root=None):
         self.tree, self.s, self.rank, self.tol = tree, s, rank, tol
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.top_level = top_level   # levels L..top_level are compressed; top_level 1 => also the root
-        L, r = tree.depth, rank
-        self.geometry = tree_geometry(tree, r, self.device)
-        lib = _native.lib()
+        r = rank
+        self.specs = specs if specs is not None else tree_level_specs(tree, r)
+        self.with_root = (self.specs[-1][0] == 1) if with_root is None else with_root
         dev, f64 = self.device, torch.float64
-        self.levels = [None] * (L + 1)
-        ws = 0
-        for level in range(L, top_level - 1, -1):
-            g = self.geometry[level]
+        lib = _native.lib()
+        from .factorization import LevelGeometry
+        self.geometry, self.first_box, self.levels = {}, {}, {}
+        ws, lift_rows = 0, []
+        for level, begins, first in self.specs:
+            g = LevelGeometry(begins, dev)
+            self.geometry[level], self.first_box[level] = g, first
             self.levels[level] = (torch.empty(g.total_rows, r, dtype=f64, device=dev),
                                   torch.empty(g.total_rows, r, dtype=f64, device=dev),
                                   torch.empty(g.sq_total, dtype=f64, device=dev))
             sz = _size_t()
             _native.check(lib.hbs_level_workspace_bytes(g.nbox, g.max_rows, s, r, ctypes.byref(sz)), "workspace")
             ws = max(ws, sz.value)
+            lift_rows.append(g.nbox * r)
+        self.geometry[0] = LevelGeometry(np.array([0, 2 * r], dtype=np.int64), dev)
         sz = _size_t()
         _native.check(lib.hbs_root_workspace_bytes(2 * r, s, ctypes.byref(sz)), "workspace")
         ws = max(ws, sz.value)
         self.workspace = torch.empty(ws // 8 + 1, dtype=f64, device=dev)
         self.workspace_bytes = ws
-        # lifted quadruples, ping-pong: level l writes 2^l * r rows
-        big = (1 << L) * r
-        self.lift = [[torch.empty(rows, s, dtype=f64, device=dev) for _ in range(4)]
-                     for rows in (big, max(big // 2, 2 * r))]
-        nstat = sum(2 * (1 << lv) for lv in range(top_level, L + 1)) + 1
+        # lifted quadruples, ping-pong between consecutive levels
+        sizes = [max(lift_rows[0::2]), max(lift_rows[1::2] or [1])]
+        self.lift = [[torch.empty(rows, s, dtype=f64, device=dev) for _ in range(4)] for rows in sizes]
+        nstat = sum(2 * self.geometry[lv].nbox for lv, _, _ in self.specs) + 1
         self.status = torch.zeros(nstat, dtype=torch.int32, device=dev)
         self.root = torch.empty(2 * r, 2 * r, dtype=f64, device=dev)
-        self.top_quad = None   # lifted quadruple feeding level top_level - 1 (multi-GPU hand-off)
+        self.top_quad = None
 
     def _status_slices(self):
         out, off = {}, 0
-        for level in range(self.tree.depth, self.top_level - 1, -1):
-            n = 2 * (1 << level)
+        for level, _, _ in self.specs:
+            n = 2 * self.geometry[level].nbox
             out[level] = self.status[off:off + n]
             off += n
         out[0] = self.status[off:off + 1]
@@ -159,10 +179,10 @@ class CompressPlan:
         """Enqueue the level sweep (compress.py:250-279) on `stream`."""
         lib = _native.lib()
         st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        L, r, s = self.tree.depth, self.rank, self.s
+        r, s = self.rank, self.s
         stat = self._status_slices()
         quad = (omega, psi, y, z)
-        for idx, level in enumerate(range(L, self.top_level - 1, -1)):
+        for idx, (level, _, _) in enumerate(self.specs):
             g = self.geometry[level]
             u, v, d = self.levels[level]
             out = self.lift[idx % 2]
@@ -175,39 +195,57 @@ class CompressPlan:
             _native.check(rc, f"hbs_compress_level(level {level})")
             rows = g.nbox * r
             quad = tuple(m[:rows] for m in out)
+        if not self.specs:
+            quad = (omega, psi, y, z)
         self.top_quad = quad
-        if self.top_level == 1:
-            g0 = self.geometry[0]
-            rc = lib.hbs_compress_root(g0.row_begin.data_ptr(), g0.sq_off.data_ptr(), 2 * r, s, self.tol,
-                                       quad[0].data_ptr(), quad[2].data_ptr(), self.root.data_ptr(),
-                                       self.workspace.data_ptr(), self.workspace_bytes, stat[0].data_ptr(), st)
-            _native.check(rc, "hbs_compress_root")
+        if self.with_root:
+            self.run_root(quad[0], quad[2], stream=st)
 
-    def raise_for_status(self):
-        """One device->host read of all per-box statuses; raise like the
-        reference for the first failing node in sweep order."""
+    def run_root(self, omega_root, y_root, stream=None):
+        """Root core D_root = Y_root Omega_root^+ (compress.py:230-233)."""
+        lib = _native.lib()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        g0 = self.geometry[0]
+        rc = lib.hbs_compress_root(g0.row_begin.data_ptr(), g0.sq_off.data_ptr(), 2 * self.rank, self.s, self.tol,
+                                   omega_root.data_ptr(), y_root.data_ptr(), self.root.data_ptr(),
+                                   self.workspace.data_ptr(), self.workspace_bytes, self._status_slices()[0].data_ptr(),
+                                   st)
+        _native.check(rc, "hbs_compress_root")
+
+    def first_failure(self):
+        """(level, node id) of the first failing box in sweep order, or None
+        (one device->host read of all statuses)."""
         host = self.status.cpu().numpy()
         if not host.any():
-            return
+            return None
         off = 0
-        for level in range(self.tree.depth, self.top_level - 1, -1):
-            nbox = 1 << level
+        for level, _, _ in self.specs:
+            nbox = self.geometry[level].nbox
             blk = host[off:off + 2 * nbox].reshape(2, nbox)
             off += 2 * nbox
             bad = np.nonzero(blk.any(axis=0))[0]
             if bad.size:
-                j = int(bad[0])
-                nid = (1 << level) - 1 + j
-                raise IllConditionedProbeError(
-                    f"node {nid} (level {level}): probe matrix is rank deficient within tolerance "
-                    f"{self.tol:g}; increase the probe count s", node_id=nid, level=level)
-        if self.top_level == 1 and host[off]:
-            raise IllConditionedProbeError(
-                f"node 0 (level 0): probe matrix is rank deficient within tolerance {self.tol:g}; "
-                "increase the probe count s", node_id=0, level=0)
+                return level, (1 << level) - 1 + self.first_box[level] + int(bad[0])
+        if self.with_root and host[off]:
+            return 0, 0
+        return None
+
+    def raise_for_status(self):
+        """Raise like the reference for the first failing node in sweep order."""
+        fail = self.first_failure()
+        if fail is not None:
+            raise_ill_conditioned(*fail, self.tol)
 
     def factorization(self) -> HbsFactorization:
-        return HbsFactorization.from_device(self.tree, self.rank, self.geometry, self.levels, self.root)
+        geo = [self.geometry[level] for level in range(self.tree.depth + 1)]
+        levels = [None] + [self.levels[level] for level in range(1, self.tree.depth + 1)]
+        return HbsFactorization.from_device(self.tree, self.rank, geo, levels, self.root)
+
+
+def raise_ill_conditioned(level, node_id, tol):
+    raise IllConditionedProbeError(
+        f"node {node_id} (level {level}): probe matrix is rank deficient within tolerance {tol:g}; "
+        "increase the probe count s", node_id=node_id, level=level)
 
 
 def _check_configuration(tree: ClusterTree, s: int, r: int):
@@ -251,18 +289,6 @@ def _charge_madds(tree: ClusterTree, s: int, r: int):
             total += cnt * (flops.node_compress_madds(int(rows), s, r) + flops.lift_madds(int(rows), s, r))
     total += flops.root_madds(2 * r, s)
     flops.add_madds(total)
-
-
-_PLANS = {}
-
-
-def get_plan(tree: ClusterTree, s: int, r: int, tol: float, device) -> CompressPlan:
-    key = (tree.n, tree.leaf_threshold, s, r, tol, str(device))
-    plan = _PLANS.get(key)
-    if plan is None:
-        _PLANS.clear()          # keep at most one plan's buffers alive
-        plan = _PLANS[key] = CompressPlan(tree, s, r, tol, device)
-    return plan
 
 
 def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: CompressionConfig,
