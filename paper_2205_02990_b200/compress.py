@@ -159,7 +159,7 @@ class CompressPlan:
         self.workspace = torch.empty(ws // 8 + 1, dtype=f64, device=dev)
         self.workspace_bytes = ws
         # lifted quadruples, ping-pong between consecutive levels
-        sizes = [max(lift_rows[0::2]), max(lift_rows[1::2] or [1])]
+        sizes = [max(lift_rows[0::2] or [1]), max(lift_rows[1::2] or [1])]
         self.lift = [[torch.empty(rows, s, dtype=f64, device=dev) for _ in range(4)] for rows in sizes]
         nstat = sum(2 * self.geometry[lv].nbox for lv, _, _ in self.specs) + 1
         self.status = torch.zeros(nstat, dtype=torch.int32, device=dev)

@@ -59,21 +59,27 @@ struct LevelWs {
   double* P[2];   // Y P and Z Q
   double* G1; double* M3; double* M4; double* E1; double* E2;
   double* gscratch;
+  bool fused;
+  // where the solve results live after factor_and_solve
+  const double* Xp[2]; int ldX; int64_t strideX;   // Y Omega^+ / Z Psi^+
+  const double* Pp[2]; int ldP; int64_t strideP;   // Y P / Z Q
 };
 
 size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bool root_only) {
   const size_t nb = (size_t)nbox;
   const int npanel = (nr + kNB - 1) / kNB;
   const int sides = root_only ? 1 : 2;
+  w.fused = fused_fits(s, nr);
   for (int sd = 0; sd < 2; ++sd) {
     const bool on = sd < sides;
+    // vt doubles as the fused kernel's Y Q buffer (rows x s per box)
     w.vt[sd] = on ? c.take<double>(nb * nr * s) : nullptr;
-    w.R[sd] = on ? c.take<double>(nb * nr * nr) : nullptr;
-    w.tau[sd] = on ? c.take<double>(nb * nr) : nullptr;
+    w.R[sd] = (on && !w.fused) ? c.take<double>(nb * nr * nr) : nullptr;
+    w.tau[sd] = (on && !w.fused) ? c.take<double>(nb * nr) : nullptr;
     w.T[sd] = on ? c.take<double>(nb * npanel * kNB * kNB) : nullptr;
-    w.Rinv[sd] = on ? c.take<double>(nb * npanel * kNB * kNB) : nullptr;
-    w.X[sd] = on ? c.take<double>(nb * nr * nr) : nullptr;
-    w.P[sd] = (on && !root_only) ? c.take<double>(nb * nr * r) : nullptr;
+    w.Rinv[sd] = on ? c.take<double>(nb * (npanel + 1) * kNB * kNB) : nullptr;   // + scratch block
+    w.X[sd] = (on && !w.fused) ? c.take<double>(nb * nr * nr) : nullptr;
+    w.P[sd] = (on && !root_only && !w.fused) ? c.take<double>(nb * nr * r) : nullptr;
   }
   if (!root_only) {
     w.G1 = c.take<double>(nb * r * nr);
@@ -118,6 +124,38 @@ int gemm(const LevelGeo& geo, BDim M, BDim N, BDim K, int mmax, int nmax, BOpera
 int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int nsides,
                      const double* om0, const double* om1, const double* y0, const double* y1,
                      LevelWs& w, int32_t* status, double* root_out, cudaStream_t st) {
+  const int npanel_f = (nr + kNB - 1) / kNB;
+  if (w.fused) {
+    FusedArgs f;
+    std::memset(&f, 0, sizeof(f));
+    f.geo = geo; f.s = s; f.n_max = nr; f.tol = tol;
+    const double* oms[2] = {om0, om1};
+    const double* ys[2] = {y0, y1};
+    for (int sd = 0; sd < nsides; ++sd) {
+      FusedSide& S = f.side[sd];
+      S.om = oms[sd]; S.om_c_rb = s;
+      S.y = ys[sd]; S.y_c_rb = s;
+      S.yq = w.vt[sd]; S.yq_stride = (int64_t)nr * s;
+      S.t = w.T[sd]; S.t_stride = (int64_t)npanel_f * kNB * kNB;
+      S.rinv = w.Rinv[sd]; S.rinv_stride = (int64_t)(npanel_f + 1) * kNB * kNB;
+      S.status = status + sd * geo.nbox;
+      w.Xp[sd] = w.vt[sd];
+      w.Pp[sd] = w.vt[sd] + (s - r);
+    }
+    w.ldX = s; w.strideX = (int64_t)nr * s;
+    w.ldP = s; w.strideP = (int64_t)nr * s;
+    HBS_TRY(launch_probe_fused(f, nsides, st));
+    g_timer.mark(); g_timer.mark(); g_timer.mark();   // (QR, panel factors and apply are one kernel)
+    if (root_out) {
+      if (cudaMemcpy2DAsync(root_out, nr * sizeof(double), w.vt[0], s * sizeof(double), nr * sizeof(double), nr,
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return kErrCuda;
+    }
+    return kOk;
+  }
+  for (int sd = 0; sd < nsides; ++sd) { w.Xp[sd] = w.X[sd]; w.Pp[sd] = w.P[sd]; }
+  w.ldX = nr; w.strideX = (int64_t)nr * nr;
+  w.ldP = r; w.strideP = (int64_t)nr * r;
   GeqrfArgs g;
   std::memset(&g, 0, sizeof(g));
   g.geo = geo; g.mode = kGeqrfFactor;
@@ -207,7 +245,7 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   double* outs[2] = {u, v};
   for (int sd = 0; sd < 2; ++sd) {
     GeqrfSide& S = g.side[sd];
-    S.src = w.P[sd]; S.src_c_rb = 0; S.src_c_b = (int64_t)nr * r; S.src_rs = r; S.src_cs = 1;
+    S.src = w.Pp[sd]; S.src_c_rb = 0; S.src_c_b = w.strideP; S.src_rs = w.ldP; S.src_cs = 1;
     S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
   HBS_TRY(launch_hqr(g, 2, st));
@@ -220,8 +258,8 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   const BOperand Vt = op(v, r, 0, 0, r, false, true);
   const BOperand Vn = op(v, r, 0, 0, r, false, false);
   const int64_t sqs = (int64_t)nr * nr, rs = (int64_t)r * nr;
-  const BOperand Xn = op(w.X[0], 0, sqs, 0, nr, false, false);
-  const BOperand Wt = op(w.X[1], 0, sqs, 0, nr, false, true);
+  const BOperand Xn = op(w.Xp[0], 0, w.strideX, 0, w.ldX, false, false);
+  const BOperand Wt = op(w.Xp[1], 0, w.strideX, 0, w.ldX, false, true);
   const BOperand G1 = op(w.G1, 0, rs, 0, nr, false, false);
   const BOperand M3 = op(w.M3, 0, (int64_t)r * r, 0, r, false, false);
   const BOperand M4 = op(w.M4, 0, rs, 0, nr, false, false);

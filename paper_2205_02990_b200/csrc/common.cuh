@@ -29,9 +29,11 @@ HBS_DEV int box_rows(const LevelGeo& g, int64_t b) {
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
 // Fragment ownership (lane = 4*g + t): A(g, t); B(t, g); C(g, 2t), C(g, 2t+1).
 HBS_DEV void dmma8x8x4(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  // not volatile: pure register semantics, so the compiler may hoist the
+  // operand loads of later k-steps above earlier MMAs.
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
 HBS_DEV double warp_sum(double v) {

@@ -27,7 +27,9 @@ __device__ long long g_hqr_trace[256];
 __device__ int g_hqr_trace_mode = 0;   // record only kernels of this mode
 #define HQR_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && args.mode == g_hqr_trace_mode) g_hqr_trace[i] = clock64(); } while (0)
 #define HQR_STEP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0) g_hqr_trace[64 + (i)] = clock64(); } while (0)
+#define FUSED_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0) g_hqr_trace[128 + (i)] = clock64(); } while (0)
 #else
+#define FUSED_MARK(i) do { } while (0)
 #define HQR_MARK(i) do { } while (0)
 #define HQR_STEP(i) do { } while (0)
 #endif
@@ -78,12 +80,23 @@ HBS_DEV double cfrag_to_bfrag(const double (&acc)[NF][2], int kk, int lane) {
   return (g & 1) ? v1 : v0;
 }
 
+// Warp-group synchronisation: NTG == 0 means the whole CTA (__syncthreads),
+// otherwise named barrier 1 over the first NTG threads.
+template <int NTG>
+HBS_DEV void gsync() {
+  if (NTG == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;\n" ::"n"(NTG) : "memory");
+}
+template <int NTG>
+HBS_DEV int gthreads() { return NTG == 0 ? (int)blockDim.x : NTG; }
+
 // A(j0:m, cb:ce) <- (I - V op(T) V^T) A(j0:m, cb:ce), V = panel j0 (nbp cols),
 // op(T) = T^T when trans (dgeqrf trailing update, H^T from the left), else T
 // (dorgqr).  T in smem (kP x kLdT).  mpad = rows rounded up to 8 (zero rows).
+template <int NTG>
 HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp, const double* T, bool trans,
-                                   int cb, int ce) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+                                   int cb, int ce, int ldt = kLdT, int warp_base = 0) {
+  const int warp = (threadIdx.x >> 5) - warp_base, lane = threadIdx.x & 31, nw = gthreads<NTG>() >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int nstrip = (ce - cb + 7) >> 3;
   for (int sidx = warp; sidx < nstrip; sidx += nw) {
@@ -112,7 +125,7 @@ HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
         const int row = 8 * f + g, col = kk + t;
-        const double av = trans ? T[col * kLdT + row] : T[row * kLdT + col];
+        const double av = trans ? T[col * ldt + row] : T[row * ldt + col];
         dmma8x8x4(w2[f][0], w2[f][1], av, bv);
       }
     }
@@ -171,12 +184,12 @@ HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp
 // form the compact-WY dots v_c . v_j on the fly (G8); after the 8 steps the
 // sub-panel's block reflector is applied to the rest of the panel on the
 // tensor cores, so only 8 warps ever contend for issue during a step.
-template <int MR>
+template <int MR, int NTG>
 HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
                           double* s_beta, uint64_t* bar, unsigned parity, double* G8, double* T8,
                           double* wpart, double* wfin) {
   constexpr int kSub = 8;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = gthreads<NTG>() >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
   for (int cs = j0; cs < j0 + nbp; cs += kSub) {
@@ -275,13 +288,13 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
       for (int k = 0; k < MR; ++k)
         if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
     }
-    __syncthreads();
+    gsync<NTG>();
     if (threadIdx.x == 0) HQR_STEP(40 + (jq >> 3) * 4);
     // finalise the sub-panel: v tails = x * scale, diagonal = beta
     for (int q = 0; q < nsub; ++q) {
       const int c = cs + q;
       const double sc = s_scale[c];
-      for (int i = c + threadIdx.x; i < m; i += blockDim.x) {
+      for (int i = c + threadIdx.x; i < m; i += gthreads<NTG>()) {
         if (i > c) A[i + c * lda] *= sc;
         else A[i + c * lda] = s_beta[c];
       }
@@ -306,7 +319,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
           for (int cc = 0; cc < kSub; ++cc) T8[lane * kSub + cc] = trow[cc];
         }
       }
-      __syncthreads();   // finalised V visible
+      gsync<NTG>();   // finalised V visible
       if (threadIdx.x == 0) HQR_STEP(41 + (jq >> 3) * 4);
       const int kspan = round_up(m - cs, 4);
       const int nsplit = 4;
@@ -332,10 +345,10 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
           wpart[ws * 192 + g * 24 + 8 * f + 2 * t + 1] = w[f][1];
         }
       }
-      __syncthreads();
+      gsync<NTG>();
       if (threadIdx.x == 0) HQR_STEP(42 + (jq >> 3) * 4);
       // W' = T8^T (sum of partials)  (8 x 24)
-      for (int e = threadIdx.x; e < 192; e += blockDim.x) {
+      for (int e = threadIdx.x; e < 192; e += gthreads<NTG>()) {
         const int q = e / 24, cc = e % 24;
         double acc = 0.0;
 #pragma unroll
@@ -346,7 +359,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
         }
         wfin[e] = acc;
       }
-      __syncthreads();
+      gsync<NTG>();
       // X_rest(rows cs.., c1..c2) -= V_sub W'
       const int nrb = (round_up(m, 8) - cs + 7) >> 3;
       for (int u = warp; u < nrb * 3; u += nw) {
@@ -367,14 +380,15 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
         if (col + 1 < c2) A[i + (col + 1) * lda] = c1v;
       }
     }
-    __syncthreads();
+    gsync<NTG>();
     if (threadIdx.x == 0) HQR_STEP(43 + (jq >> 3) * 4);
   }
 }
 
 // G = V_p^T V_p (32 x 32) on the tensor cores; warp w < 16 computes one 8x8 block.
+template <int NTG>
 HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = gthreads<NTG>() >> 5;
   const int g = lane >> 2, t = lane & 3;
   for (int blk = warp; blk < 16; blk += nw) {
     const int fi = blk >> 2, fj = blk & 3;
@@ -402,10 +416,11 @@ HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double
 //   8x8 diagonal blocks by the column recurrence T(0:c, c) = -tau_c T(0:c,0:c) G(0:c, c)
 //   (four warps in parallel), then the block formula
 //   T = [[T1, -T1 G12 T2], [0, T2]]  for 8+8 -> 16 and 16+16 -> 32.
+template <int NTG>
 HBS_DEV void form_t(double* T, double* scratch, const double* G, const double* s_tau, int j0, int nbp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < kP * kLdT; e += blockDim.x) T[e] = 0.0;
-  __syncthreads();
+  for (int e = threadIdx.x; e < kP * kLdT; e += gthreads<NTG>()) T[e] = 0.0;
+  gsync<NTG>();
   if (warp < 4 && lane < 8) {
     const int base = 8 * warp, a = base + lane;
     double trow[8];
@@ -422,28 +437,28 @@ HBS_DEV void form_t(double* T, double* scratch, const double* G, const double* s
 #pragma unroll
     for (int c = 0; c < 8; ++c) T[a * kLdT + base + c] = trow[c];
   }
-  __syncthreads();
+  gsync<NTG>();
   // combine: width 8 -> 16 (two pairs), then 16 -> 32
   for (int w = 8; w < kP; w *= 2) {
     const int npair = kP / (2 * w);
     // X = G12 T2 for every pair  (w x w each)
-    for (int e = threadIdx.x; e < npair * w * w; e += blockDim.x) {
+    for (int e = threadIdx.x; e < npair * w * w; e += gthreads<NTG>()) {
       const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
       const int o1 = 2 * w * pr, o2 = o1 + w;
       double acc = 0.0;
       for (int q = 0; q <= c; ++q) acc = fma(G[(o1 + i) * kLdT + o2 + q], T[(o2 + q) * kLdT + o2 + c], acc);
       scratch[e] = acc;
     }
-    __syncthreads();
+    gsync<NTG>();
     // T12 = -T1 X
-    for (int e = threadIdx.x; e < npair * w * w; e += blockDim.x) {
+    for (int e = threadIdx.x; e < npair * w * w; e += gthreads<NTG>()) {
       const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
       const int o1 = 2 * w * pr, o2 = o1 + w;
       double acc = 0.0;
       for (int q = i; q < w; ++q) acc = fma(T[(o1 + i) * kLdT + o1 + q], scratch[pr * w * w + q * w + c], acc);
       T[(o1 + i) * kLdT + o2 + c] = -acc;
     }
-    __syncthreads();
+    gsync<NTG>();
   }
 }
 
@@ -538,18 +553,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
     const int j0 = p * kP, nbp = min(kP, n - j0);
     double* T = Tbase + (args.mode == kGeqrfOrtho ? p * kP * kLdT : 0);
     HQR_MARK(2 + 4 * p);
-    panel_factor<MR>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr, Tscr + 64, G,
+    panel_factor<MR, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr, Tscr + 64, G,
                      Tscr + 128);
     HQR_MARK(3 + 4 * p);
-    panel_gram(A, lda, m, j0, nbp, G);
+    panel_gram<0>(A, lda, m, j0, nbp, G);
     __syncthreads();
-    form_t(T, Tscr, G, s_tau, j0, nbp);
+    form_t<0>(T, Tscr, G, s_tau, j0, nbp);
     if (args.mode == kGeqrfFactor) {
       double* tout = S.t + (size_t)b * S.t_stride + (size_t)p * kP * kP;
       for (int e = threadIdx.x; e < kP * kP; e += blockDim.x) tout[e] = T[(e / kP) * kLdT + e % kP];
     }
     HQR_MARK(4 + 4 * p);
-    if (j0 + kP < n) block_reflector_apply(A, lda, round_up(m, 8), j0, nbp, T, true, j0 + kP, n);
+    if (j0 + kP < n) block_reflector_apply<0>(A, lda, round_up(m, 8), j0, nbp, T, true, j0 + kP, n);
     HQR_MARK(5 + 4 * p);
     __syncthreads();
   }
@@ -592,7 +607,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
     const int j0 = p * kP, nbp = min(kP, n - j0);
     const double* T = Tbase + p * kP * kLdT;
     // columns right of the panel already hold Q; apply the block reflector
-    if (j0 + kP < n) block_reflector_apply(A, lda, mp8, j0, nbp, T, false, j0 + kP, n);
+    if (j0 + kP < n) block_reflector_apply<0>(A, lda, mp8, j0, nbp, T, false, j0 + kP, n);
     // S = T V1^T (32 x 32) -> G, one 8x8 fragment per warp (V1 = V(j0:j0+32, :))
     {
       const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -730,6 +745,350 @@ int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream) {
     case 9: case 10: return launch_hqr_mr<10>(args, nsides, stream);
     case 11: case 12: return launch_hqr_mr<12>(args, nsides, stream);
     case 13: case 14: case 15: case 16: return launch_hqr_mr<16>(args, nsides, stream);
+    default: return kErrUnsupported;
+  }
+}
+
+
+// ============================================================================
+// Fused probe QR + apply-Q + solve.
+// ============================================================================
+namespace {
+
+// inverse of the 32x32 upper-triangular block R(j0:j0+32, j0:j0+32) (in A)
+// into out (32 x kLdT) by the group: 8x8 diagonal blocks by lane-per-column
+// back substitution, then inv([[A,B],[0,C]]) = [[A^-1, -A^-1 B C^-1],[0, C^-1]].
+template <int NTG, int BAR>
+HBS_DEV void ysync() { asm volatile("bar.sync %0, %1;\n" ::"n"(BAR), "n"(NTG) : "memory"); }
+
+// Inverse of the 32x32 upper-triangular block R(j0:j0+32, j0:j0+32) (in A),
+// by the warp group starting at warp `wb` (NTG threads, named barrier BAR):
+// 8x8 diagonal blocks by lane-per-column back substitution, then
+// inv([[A,B],[0,C]]) = [[A^-1, -A^-1 B C^-1],[0, C^-1]] for 8+8 and 16+16.
+// out / scratch may live in global memory (row-major, ld 32 / 256 doubles).
+template <int NTG, int BAR>
+HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* out, double* scratch, int wb) {
+  const int tid = threadIdx.x - 32 * wb, warp = tid >> 5, lane = tid & 31;
+  auto R = [&](int i, int c) -> double {
+    if (i >= nbp || c >= nbp) return i == c ? 1.0 : 0.0;
+    return A[(j0 + i) + (j0 + c) * lda];
+  };
+  for (int e = tid; e < kP * kP; e += NTG) out[e] = 0.0;
+  ysync<NTG, BAR>();
+  if (warp < 4 && lane < 8) {
+    const int base = 8 * warp, c = lane;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      x[i] = x[i] / R(base + i, base + i);
+#pragma unroll
+      for (int k = 0; k < i; ++k) x[k] = fma(-R(base + k, base + i), x[i], x[k]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[(base + i) * kP + base + c] = x[i];
+  }
+  __threadfence_block();
+  ysync<NTG, BAR>();
+  for (int w = 8; w < kP; w *= 2) {
+    const int npair = kP / (2 * w);
+    for (int e = tid; e < npair * w * w; e += NTG) {   // X = B C^-1
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = 0; q <= c; ++q) acc = fma(R(o1 + i, o2 + q), out[(o2 + q) * kP + o2 + c], acc);
+      scratch[e] = acc;
+    }
+    __threadfence_block();
+    ysync<NTG, BAR>();
+    for (int e = tid; e < npair * w * w; e += NTG) {   // -A^-1 X
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = i; q < w; ++q) acc = fma(out[(o1 + i) * kP + o1 + q], scratch[pr * w * w + q * w + c], acc);
+      out[(o1 + i) * kP + o2 + c] = -acc;
+    }
+    __threadfence_block();
+    ysync<NTG, BAR>();
+  }
+}
+
+}  // namespace
+
+template <int MR>
+__global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
+  extern __shared__ double smem[];
+  const int side = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const FusedSide& S = args.side[side];
+  const int nb = box_rows(args.geo, b);
+  const int m = args.s, n = nb, s = args.s;
+  const int lda = args.lda;
+  const int mpad = round_up(m, 32);
+  const int npanel = (n + kP - 1) / kP;
+  const int64_t rb = args.geo.row_begin[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  double* s_tau = smem;
+  double* s_scale = s_tau + args.n_max;
+  double* s_beta = s_scale + args.n_max;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + args.n_max);   // 32 step barriers
+  uint64_t* s_ready = s_bar + kP;                                          // 16 panel-ready + 1 R-ready
+  double* G = smem + round_up(3 * args.n_max + kP + 32, 2);
+  double* Tscr = G + kP * kLdT;
+  double* T = Tscr + 384;
+  double* A = T + round_up(kP * kLdT, 2);
+
+  // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1
+  const double* src = S.om + S.om_c_rb * rb;
+  for (int j = 0; j < n; ++j)
+    for (int i = threadIdx.x; i < mpad; i += blockDim.x) {
+      const bool ok = i < m;
+      cp_async8(&A[i + j * lda], ok ? src + (int64_t)j * s + i : src, ok);
+    }
+  cp_async_commit();
+  if (threadIdx.x < kP + 32) mbar_init(&s_bar[threadIdx.x], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  cp_async_wait<0>();
+  __syncthreads();
+
+  double* tglob = S.t + (size_t)b * S.t_stride;
+  double* rglob = S.rinv + (size_t)b * S.rinv_stride;
+  if (threadIdx.x == 0) FUSED_MARK(0);
+  // s_ready[p] (p < 16): panel p factored (P -> Y);  s_ready[16 + p]: far
+  // trailing update of panel p done (Y -> P); p < 8 for the latter.
+  if (warp < 8) {
+    // ------------------------------------------------------------ group P
+    for (int p = 0; p < npanel; ++p) {
+      const int j0 = p * kP, nbp = min(kP, n - j0);
+      if (p >= 2) mbar_wait(&s_ready[16 + p - 2], 0);   // panels <= p-2 applied to my columns by group Y
+      if (p >= 1) {                                      // look-ahead: apply panel p-1 to panel p's columns
+        const int jp = j0 - kP;
+        block_reflector_apply<256>(A, lda, round_up(m, 8), jp, kP, tglob + (size_t)(p - 1) * kP * kP, true, j0,
+                                   j0 + nbp, kP);
+        gsync<256>();
+      }
+      panel_factor<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr,
+                            Tscr + 64, G, Tscr + 128);
+      panel_gram<256>(A, lda, m, j0, nbp, G);
+      gsync<256>();
+      form_t<256>(T, Tscr, G, s_tau, j0, nbp);
+      for (int e = threadIdx.x; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
+      __threadfence_block();
+      gsync<256>();
+      if (threadIdx.x == 0) { mbar_arrive(&s_ready[p]); FUSED_MARK(1 + 2 * p); }
+    }
+    if (threadIdx.x < 32) {  // sigma screen on diag(R)
+      double lo = INFINITY, hi = 0.0;
+      for (int j = threadIdx.x; j < n; j += 32) {
+        const double d = fabs(A[j + j * lda]);
+        lo = fmin(lo, d);
+        hi = fmax(hi, d);
+      }
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      if (threadIdx.x == 0) {
+        const bool bad = !(hi > 0.0) || lo < args.tol * hi || !isfinite(hi);
+        S.status[b] = bad ? kBoxIllConditioned : kBoxOk;
+        FUSED_MARK(20);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- group Y
+  const int yw = warp - 8;
+  const double* y0 = S.y + S.y_c_rb * rb;
+  double* yq = S.yq + (size_t)b * S.yq_stride;
+  const int spad = round_up(s, 8);
+  const int ngroups = (nb + 7) >> 3;
+  for (int p = 0; p < npanel; ++p) {
+    const int j0 = p * kP, nbp = min(kP, n - j0), kb = j0 & ~7;
+    mbar_wait(&s_ready[p], 0);
+    const double* tp = tglob + (size_t)p * kP * kP;
+    // far trailing update: panel p applied to the columns beyond panel p+1
+    if (j0 + 2 * kP < n) {
+      block_reflector_apply<256>(A, lda, round_up(m, 8), j0, nbp, tp, true, j0 + 2 * kP, n, kP, 8);
+      ysync<256, 2>();
+      if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]);
+    }
+    // R's diagonal block p is final: its inverse for the solve
+    tri_inverse32<256, 2>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, rglob + (size_t)npanel * kP * kP, 8);
+    for (int rg = yw; rg < ngroups; rg += 8) {
+      const int row = 8 * rg + g;
+      const bool rok = row < nb;
+      const double* srow = (p == 0 ? y0 : yq) + (size_t)row * s;
+      double* drow = yq + (size_t)row * s;
+      // GEMM1: W = Y(:, kb:) V_p   (8 x 32); A-fragment loads issued 32 columns ahead
+      double w[4][2] = {};
+      for (int kc = kb; kc < spad; kc += 32) {
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int col = kc + 4 * u + t;
+          av[u] = (rok && col < s && kc + 4 * u < spad) ? __ldcg(srow + col) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = kc + 4 * u;
+          if (k >= spad) break;
+          if (k < j0 + kP) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) dmma8x8x4(w[f][0], w[f][1], av[u], vval(A, lda, j0, nbp, k + t, 8 * f + g));
+          } else {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+              const double bv = (8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0;
+              dmma8x8x4(w[f][0], w[f][1], av[u], bv);
+            }
+          }
+        }
+      }
+      // GEMM2: W2 = W T_p
+      double tb[kP / 4][4];
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) tb[kk / 4][f] = __ldg(tp + (kk + t) * kP + 8 * f + g);
+      double w2[4][2] = {};
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        const double a = cfrag_to_afrag<4>(w, kk, lane);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) dmma8x8x4(w2[f][0], w2[f][1], a, tb[kk / 4][f]);
+      }
+      double a3[kP / 4];
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) a3[kk / 4] = -cfrag_to_afrag<4>(w2, kk, lane);
+      // GEMM3: Y(:, kb:) -= W2 V_p^T  (first panel also copies columns < kb);
+      // C-fragment loads issued 4 column blocks ahead
+      if (p == 0) {
+        for (int c = 2 * t; c < kb; c += 8)
+          if (rok) *reinterpret_cast<double2*>(drow + c) = __ldcg(reinterpret_cast<const double2*>(srow + c));
+      }
+      for (int nc = kb; nc < spad; nc += 32) {
+        double2 cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = nc + 8 * u + 2 * t;
+          cv[u] = (rok && col < s) ? __ldcg(reinterpret_cast<const double2*>(srow + col)) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int n0 = nc + 8 * u;
+          if (n0 >= spad) break;
+          if (n0 < j0 + kP) {
+#pragma unroll
+            for (int kk = 0; kk < kP; kk += 4)
+              dmma8x8x4(cv[u].x, cv[u].y, a3[kk / 4], vval(A, lda, j0, nbp, n0 + g, kk + t));
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < kP; kk += 4) {
+              const double bv = (kk + t < nbp) ? A[(n0 + g) + (j0 + kk + t) * lda] : 0.0;
+              dmma8x8x4(cv[u].x, cv[u].y, a3[kk / 4], bv);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = nc + 8 * u + 2 * t;
+          if (rok && col < s && nc + 8 * u < spad) *reinterpret_cast<double2*>(drow + col) = cv[u];
+        }
+      }
+      __syncwarp();
+    }
+    if (yw == 0 && lane == 0) FUSED_MARK(30 + p);
+  }
+  // blocked back substitution X R^T = Y Q1, in place in YQ (columns < n)
+  ysync<256, 2>();
+  if (yw == 0 && lane == 0) FUSED_MARK(40);
+  for (int rg = yw; rg < ngroups; rg += 8) {
+    const int row = 8 * rg + g;
+    const bool rok = row < nb;
+    double* drow = yq + (size_t)row * s;
+    for (int blk = npanel - 1; blk >= 0; --blk) {
+      const int i0 = blk * kP, c0 = i0 + kP;
+      const int kr = n > c0 ? round_up(n - c0, 4) : 0;
+      double acc[4][2];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = i0 + 8 * f + 2 * t + e;
+          acc[f][e] = (rok && c < n) ? __ldcg(drow + c) : 0.0;
+        }
+      for (int kc = 0; kc < kr; kc += 32) {
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + kc + 4 * u + t;
+          av[u] = (rok && c < n) ? -__ldcg(drow + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (kc + 4 * u >= kr) break;
+          const int c = c0 + kc + 4 * u + t;
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const int i = i0 + 8 * f + g;
+            const double bv = (i < n && c < n) ? A[i + c * lda] : 0.0;   // R(i, c), upper part
+            dmma8x8x4(acc[f][0], acc[f][1], av[u], bv);
+          }
+        }
+      }
+      const double* ri = rglob + (size_t)blk * kP * kP;
+      double xb[4][2] = {};
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        const double a = cfrag_to_afrag<4>(acc, kk, lane);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) dmma8x8x4(xb[f][0], xb[f][1], a, __ldcg(ri + (8 * f + g) * kP + kk + t));
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = i0 + 8 * f + 2 * t + e;
+          if (rok && c < n) drow[c] = xb[f][e];
+        }
+      __syncwarp();
+    }
+  }
+  if (yw == 0 && lane == 0) FUSED_MARK(41);
+}
+
+bool fused_fits(int s, int n_max) {
+  const int lda = frag_ld(round_up(s, 32));
+  const size_t d = round_up(3 * n_max + kP + 32, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) + (size_t)lda * n_max;
+  return n_max <= 16 * kP && d * sizeof(double) <= kMaxSmemBytes;
+}
+
+template <int MR>
+static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
+  args.lda = frag_ld(round_up(args.s, 32));
+  const size_t d = round_up(3 * args.n_max + kP + 32, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
+                   (size_t)args.lda * args.n_max;
+  const size_t smem = d * sizeof(double);
+  cudaFuncSetAttribute(probe_fused_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)args.geo.nbox, nsides);
+  probe_fused_kernel<MR><<<grid, 512, smem, stream>>>(args);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream) {
+  if (!fused_fits(args.s, args.n_max)) return kErrUnsupported;
+  switch ((args.s + 31) / 32) {
+    case 1: return launch_fused_mr<1>(args, nsides, stream);
+    case 2: return launch_fused_mr<2>(args, nsides, stream);
+    case 3: return launch_fused_mr<3>(args, nsides, stream);
+    case 4: return launch_fused_mr<4>(args, nsides, stream);
+    case 5: return launch_fused_mr<5>(args, nsides, stream);
+    case 6: return launch_fused_mr<6>(args, nsides, stream);
+    case 7: return launch_fused_mr<7>(args, nsides, stream);
+    case 8: return launch_fused_mr<8>(args, nsides, stream);
     default: return kErrUnsupported;
   }
 }

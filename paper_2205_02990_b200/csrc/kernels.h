@@ -65,6 +65,28 @@ size_t hqr_scratch_doubles(int m_max, int n_max, int64_t nbox);
 bool hqr_fits_smem(int m_max, int n_max, int mode);
 int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream);
 
+// ---------------------------------------------------------------- fused probe QR + apply Q + solve
+// Per (box, side): Householder QR of Omega_tau^T in shared memory (warps 0-7)
+// while warps 8-15 apply each finished panel to the box's Y rows (streamed
+// from L2) and finally solve X = (Y Q1) R^{-T}.  Output YQ (rows x s per box):
+// columns 0..n-1 hold X = Y Omega^+, columns s-r..s-1 hold Y P.
+struct FusedSide {
+  const double* om; int64_t om_c_rb;       // Omega rows of box b at om + om_c_rb*row_begin[b], ld = s
+  const double* y; int64_t y_c_rb;         // Y rows, ld = s
+  double* yq; int64_t yq_stride;           // per box rows x s (ld = s), uniform stride
+  double* t; int64_t t_stride;             // npanel x 32 x 32 compact-WY T blocks
+  double* rinv; int64_t rinv_stride;       // npanel x 32 x 32 R diagonal-block inverses
+  int32_t* status;
+};
+struct FusedArgs {
+  LevelGeo geo;
+  FusedSide side[2];
+  int s, n_max, lda;
+  double tol;
+};
+bool fused_fits(int s, int n_max);
+int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream);
+
 // ---------------------------------------------------------------- panel factors
 // Per (box, side, panel): compact-WY T block (dlarft, forward/columnwise) of
 // the reflectors j0..j0+NB-1 and the inverse of R's diagonal block.

@@ -24,6 +24,10 @@ torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 256)()
 getattr(lib, "hbs_debug_hqr_trace")(buf)
 t = list(buf)
+f = t[128:128 + 48]
+print("FUSED (cycles from start):", {"P panel ready": [f[1 + 2 * p] - f[0] for p in range(4)],
+      "P trailing done": [f[2 + 2 * p] - f[0] for p in range(4)], "P rinv done": f[20] - f[0],
+      "Y panel done": [f[30 + p] - f[0] for p in range(4)], "Y solve start": f[40] - f[0], "Y end": f[41] - f[0]})
 print("load", t[1] - t[0])
 for p in range(4):
     a = 2 + 4 * p
