@@ -105,6 +105,14 @@ int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, 
                  double tol, const double* omega, double* vt, double* r, double* tau, double* t, double* rinv,
                  double* scratch, int32_t* status, void* stream);
 
+/* Building block: batched reduced Householder QR with explicit Q -- the
+ * reference's col() (linalg.py:35-49: np.linalg.qr(b)[0][:, :r]) for every
+ * box of a level.  b and q are packed (rows x r) row-major with box b at row
+ * row_begin[b]; q may alias nothing in b.  scratch: hbs_basis_qr_scratch_bytes. */
+int hbs_basis_qr_scratch_bytes(int64_t nbox, int max_rows, int r, size_t* bytes);
+int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
+                 const double* b, double* q, double* scratch, void* stream);
+
 /* Number of CUDA kernels launched by this library so far (process-wide). */
 unsigned long long hbs_launch_counter(void);
 

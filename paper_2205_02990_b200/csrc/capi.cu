@@ -336,6 +336,29 @@ int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, 
   return launch_hqr(g, 1, static_cast<cudaStream_t>(stream));
 }
 
+int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
+                 const double* b, double* q, double* scratch, void* stream) {
+  if (nbox < 1 || max_rows < r || r < 1) return HBS_ERR_DIMENSION;
+  if (max_rows > 512) return HBS_ERR_UNSUPPORTED;
+  GeqrfArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = LevelGeo{row_begin, sq_off, nbox}; g.mode = kGeqrfOrtho;
+  g.m_fixed = 0; g.m_is_rows = 1; g.n_fixed = r; g.n_is_rows = 0;
+  g.m_max = max_rows; g.n_max = r; g.gscratch = scratch;
+  for (int sd = 0; sd < 1; ++sd) {
+    GeqrfSide& S = g.side[sd];
+    S.src = b; S.src_c_rb = r; S.src_c_b = 0; S.src_rs = r; S.src_cs = 1;
+    S.q = q; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
+  }
+  return launch_hqr(g, 1, static_cast<cudaStream_t>(stream));
+}
+
+int hbs_basis_qr_scratch_bytes(int64_t nbox, int max_rows, int r, size_t* bytes) {
+  if (!bytes) return HBS_ERR_DIMENSION;
+  *bytes = hqr_fits_smem(max_rows, r, kGeqrfOrtho) ? 0 : hqr_scratch_doubles(max_rows, r, nbox) * sizeof(double);
+  return HBS_OK;
+}
+
 int hbs_probe_qr_scratch_bytes(int64_t nbox, int max_rows, int s, size_t* bytes) {
   if (!bytes) return HBS_ERR_DIMENSION;
   *bytes = hqr_fits_smem(s, max_rows, kGeqrfFactor) ? 0 : hqr_scratch_doubles(s, max_rows, nbox) * sizeof(double);

@@ -28,8 +28,10 @@ __device__ int g_hqr_trace_mode = 0;   // record only kernels of this mode
 #define HQR_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && args.mode == g_hqr_trace_mode) g_hqr_trace[i] = clock64(); } while (0)
 #define HQR_STEP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0) g_hqr_trace[64 + (i)] = clock64(); } while (0)
 #define FUSED_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0) g_hqr_trace[128 + (i)] = clock64(); } while (0)
+#define STEP_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 32 && lane == 0) g_hqr_trace[200 + (i)] = clock64(); } while (0)
 #else
 #define FUSED_MARK(i) do { } while (0)
+#define STEP_MARK(i) do { } while (0)
 #define HQR_MARK(i) do { } while (0)
 #define HQR_STEP(i) do { } while (0)
 #endif
@@ -262,7 +264,7 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
         if (pub) {
           const double sxp = d - pn * xn_old;
           double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
-          if (!(nrm > 0.5 * sxx)) {   // cancellation: recompute exactly
+          if (!(nrm > 0.5 * sxx) || sxx == 0.0) {   // cancellation: recompute exactly
             double p = 0.0;
 #pragma unroll
             for (int k = 0; k < MR; ++k) {
@@ -383,6 +385,286 @@ HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_
     gsync<NTG>();
     if (threadIdx.x == 0) HQR_STEP(43 + (jq >> 3) * 4);
   }
+}
+
+// Whole-panel factorisation (no sub-panels).  NW warps; warp w owns panel
+// columns j0 + w + NW*u (u < CPW = 32/NW) in registers (rows j0 + lane + 32k).
+// Step j needs only pivot j: its owner publishes (column in A; tau / scale /
+// beta in smem; next-pivot norm by the expansion
+// ||x - g p||^2 = sxx - 2 g sxp + g^2 spp, recomputed exactly on
+// cancellation) and arrives on bar[j]; every other warp waits on bar[j] only.
+// Owners of retired columns form the compact-WY dots G(c, j) = v_c . v_j in
+// the same reductions, so T needs no separate Gram.  bar[] completes once per
+// panel (parity = panel & 1).
+template <int MR, int NW, int NTG>
+HBS_DEV void panel_factor_wide(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                               double* s_beta, uint64_t* bar, unsigned parity, double* G) {
+  // G(q, j) is only written for q < j < nbp; zero it so form_t never reads
+  // stale shared memory for partial panels.
+  for (int e = threadIdx.x; e < kP * kLdT; e += gthreads<NTG>()) G[e] = 0.0;
+  gsync<NTG>();
+  constexpr int CPW = 32 / NW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kc = (m - j0 + 31) >> 5;
+  double x[CPW][MR];
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int q = warp + NW * u;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) x[u][k] = (q < nbp && k < kc) ? A[(j0 + lane + 32 * k) + (j0 + q) * lda] : 0.0;
+  }
+  if (warp == 0) {  // first pivot: column j0 (warp 0, u = 0), exact norm
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < MR; ++k)
+      if (k < kc && j0 + lane + 32 * k > j0) p = fma(x[0][k], x[0][k], p);
+    p = warp_sum(p);
+    const double alpha = __shfl_sync(0xffffffffu, x[0][0], 0);
+    if (lane == 0) {
+      const Reflector h = make_reflector(alpha, p);
+      s_tau[j0] = h.tau; s_scale[j0] = h.scale; s_beta[j0] = h.beta;
+      mbar_arrive(&bar[0]);
+    }
+  }
+  for (int j = 0; j < nbp; ++j) {
+    const int jj = j0 + j;
+    const bool tr = (j == 6) && (((j + 1) % NW) == warp);
+    if (tr) STEP_MARK(0);
+    mbar_wait(&bar[j], parity);
+    if (tr) STEP_MARK(1);
+    const double tau = s_tau[jj], scale = s_scale[jj];
+    double pv[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int row = j0 + lane + 32 * k;
+      pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+    }
+    const bool pubw = (j + 1 < nbp) && (((j + 1) % NW) == warp);   // I own the next pivot
+    const int upub = (j + 1) / NW;
+    double d[CPW], r_[CPW];
+    double sxx = 0.0, spp = 0.0;
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      r_[u] = __shfl_sync(0xffffffffu, x[u][0], j);
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) a = fma(pv[k], x[u][k], a);
+      d[u] = a;
+      if (pubw && u == upub) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (j0 + lane + 32 * k > jj + 1) { sxx = fma(x[u][k], x[u][k], sxx); spp = fma(pv[k], pv[k], spp); }
+      }
+    }
+    if (tr) STEP_MARK(2);
+    double pn = 0.0, xn_old = 0.0;
+    if (pubw) {
+      pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+#pragma unroll
+      for (int u = 0; u < CPW; ++u)
+        if (u == upub) xn_old = __shfl_sync(0xffffffffu, x[u][0], j + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+      if (pubw) {
+        sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+        spp += __shfl_xor_sync(0xffffffffu, spp, o);
+      }
+    }
+    if (tr) STEP_MARK(3);
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const int q = warp + NW * u, c = j0 + q;
+      if (q >= nbp || c == jj) continue;
+      if (c < jj) {   // retired reflector: compact-WY dot v_c . v_jj
+        if (lane == 0) G[q * kLdT + j] = s_scale[c] * (r_[u] + scale * d[u]);
+        continue;
+      }
+      const double f = tau * (r_[u] + scale * d[u]), gs = f * scale;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) x[u][k] = fma(-gs, pv[k], x[u][k]);
+      if (lane == j) x[u][0] -= f;
+      if (pubw && u == upub) {
+        if (tr) STEP_MARK(4);
+        const double sxp = d[u] - pn * xn_old;
+        double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
+        if (!(nrm > 0.5 * sxx) || sxx == 0.0) {   // cancellation: recompute exactly
+          double p = 0.0;
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (k < kc && j0 + lane + 32 * k > jj + 1) p = fma(x[u][k], x[u][k], p);
+          nrm = warp_sum(p);
+        }
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[u][k];
+        if (tr) STEP_MARK(5);
+        const double alpha = __shfl_sync(0xffffffffu, x[u][0], j + 1);
+        __syncwarp();
+        if (lane == 0) {
+          const Reflector h = make_reflector(alpha, nrm);
+          s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+          if (tr) STEP_MARK(6);
+          mbar_arrive(&bar[j + 1]);
+          if (tr) STEP_MARK(7);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int q = warp + NW * u;
+    if (q < nbp) {
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (k < kc) A[(j0 + lane + 32 * k) + (j0 + q) * lda] = x[u][k];
+    }
+  }
+  gsync<NTG>();
+  for (int q = 0; q < nbp; ++q) {   // finalise: v tails = x * scale, diagonal = beta
+    const int c = j0 + q;
+    const double sc = s_scale[c];
+    for (int i = c + threadIdx.x; i < m; i += gthreads<NTG>()) {
+      if (i > c) A[i + c * lda] *= sc;
+      else A[i + c * lda] = s_beta[c];
+    }
+  }
+  gsync<NTG>();
+}
+
+// Panel factorisation with 8-lane column groups (warps 0..7 of the CTA).
+// Lane group lg = lane / 8 of warp w owns panel column q = w + 8 lg; lane
+// li = lane % 8 of the group holds rows j0 + li + 8k (k < MR8) in registers.
+// Every column-dot reduction is a 3-stage xor shuffle inside the group, and
+// the four groups of a warp reduce in the same shuffle instructions, so a
+// step costs each warp 6 shuffles instead of 10 per column (the SM's shuffle
+// throughput, not latency, limited the 32-lane layout).  Step j needs only
+// pivot j (mbarrier hand-off, as in panel_factor_wide); retired columns form
+// the compact-WY dots G(q, j) in the same reductions.
+template <int MR8, int NTG>
+HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                            double* s_beta, uint64_t* bar, unsigned parity, double* G) {
+  // G(q, j) is only written for q < j < nbp; zero it so form_t never reads
+  // stale shared memory for partial panels.
+  for (int e = threadIdx.x; e < kP * kLdT; e += gthreads<NTG>()) G[e] = 0.0;
+  gsync<NTG>();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 8) {
+    const int lg = lane >> 3, li = lane & 7, gbase = lane & 24;
+    const int q = warp + 8 * lg, c = j0 + q;
+    const bool own = q < nbp;
+    const int kc = (m - j0 + 7) >> 3;
+    double x[MR8];
+#pragma unroll
+    for (int k = 0; k < MR8; ++k) x[k] = (own && k < kc) ? A[(j0 + li + 8 * k) + c * lda] : 0.0;
+    if (warp == 0) {  // first pivot j0 = column q 0 (warp 0, group 0): exact norm
+      double p = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR8; ++k)
+        if (k < kc && li + 8 * k > 0) p = fma(x[k], x[k], p);
+      p += __shfl_xor_sync(0xffffffffu, p, 4);
+      p += __shfl_xor_sync(0xffffffffu, p, 2);
+      p += __shfl_xor_sync(0xffffffffu, p, 1);
+      const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
+      if (lane == 0) {
+        const Reflector h = make_reflector(alpha, p);
+        s_tau[j0] = h.tau; s_scale[j0] = h.scale; s_beta[j0] = h.beta;
+        mbar_arrive(&bar[0]);
+      }
+    }
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {          // row slot of the pivot: kb = j / 8 (compile time)
+      for (int jl = 0; jl < 8; ++jl) {
+        const int j = 8 * kb + jl, jj = j0 + j;
+        if (j >= nbp) break;
+        mbar_wait(&bar[j], parity);
+        const double tau = s_tau[jj], scale = s_scale[jj];
+        double pv[MR8];
+#pragma unroll
+        for (int k = 0; k < MR8; ++k) {
+          const int row = j0 + li + 8 * k;
+          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+        }
+        const bool pub = own && (q == j + 1);
+        // my value in row jj (slot kb, lane jl of my group) and in row jj+1
+        const double r = __shfl_sync(0xffffffffu, x[kb], gbase | jl);
+        const double xn_old = (jl == 7) ? __shfl_sync(0xffffffffu, x[kb < 3 ? kb + 1 : kb], gbase)
+                                        : __shfl_sync(0xffffffffu, x[kb], gbase | (jl + 1));
+        const double pn = (jl == 7) ? __shfl_sync(0xffffffffu, pv[kb < 3 ? kb + 1 : kb], gbase)
+                                    : __shfl_sync(0xffffffffu, pv[kb], gbase | (jl + 1));
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, sxx = 0.0, spp = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR8; k += 4) {
+          d0 = fma(pv[k], x[k], d0);
+          if (k + 1 < MR8) d1 = fma(pv[k + 1], x[k + 1], d1);
+          if (k + 2 < MR8) d2 = fma(pv[k + 2], x[k + 2], d2);
+          if (k + 3 < MR8) d3 = fma(pv[k + 3], x[k + 3], d3);
+        }
+        if (pub) {
+#pragma unroll
+          for (int k = 0; k < MR8; ++k)
+            if (li + 8 * k > j + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
+        }
+        double d = (d0 + d1) + (d2 + d3);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          d += __shfl_xor_sync(0xffffffffu, d, o);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+          spp += __shfl_xor_sync(0xffffffffu, spp, o);
+        }
+        if (own && c < jj) {            // retired reflector: compact-WY dot
+          if (li == 0) G[q * kLdT + j] = s_scale[c] * (r + scale * d);
+        } else if (own && c > jj) {
+          const double f = tau * (r + scale * d), gs = f * scale;
+#pragma unroll
+          for (int k = 0; k < MR8; ++k) x[k] = fma(-gs, pv[k], x[k]);
+          if (li == jl) x[kb] -= f;
+          if (pub) {
+            const double sxp = d - pn * xn_old;
+            double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
+            double p = 0.0;
+            if (!(nrm > 0.5 * sxx) || sxx == 0.0) {
+#pragma unroll
+              for (int k = 0; k < MR8; ++k)
+                if (k < kc && li + 8 * k > j + 1) p = fma(x[k], x[k], p);
+            }
+            p += __shfl_xor_sync(0x000000ffu << gbase, p, 4);
+            p += __shfl_xor_sync(0x000000ffu << gbase, p, 2);
+            p += __shfl_xor_sync(0x000000ffu << gbase, p, 1);
+            if (!(nrm > 0.5 * sxx) || sxx == 0.0) nrm = p;
+#pragma unroll
+            for (int k = 0; k < MR8; ++k)
+              if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
+            const double alpha = (jl == 7) ? __shfl_sync(0x000000ffu << gbase, x[kb < 3 ? kb + 1 : kb], gbase)
+                                           : __shfl_sync(0x000000ffu << gbase, x[kb], gbase | (jl + 1));
+            __syncwarp(0x000000ffu << gbase);
+            if (li == 0) {
+              const Reflector h = make_reflector(alpha, nrm);
+              s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+              mbar_arrive(&bar[j + 1]);
+            }
+          }
+        }
+      }
+    }
+    if (own) {
+#pragma unroll
+      for (int k = 0; k < MR8; ++k)
+        if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
+    }
+  }
+  gsync<NTG>();
+  for (int qq = 0; qq < nbp; ++qq) {   // finalise: v tails = x * scale, diagonal = beta
+    const int cc = j0 + qq;
+    const double sc = s_scale[cc];
+    for (int i = cc + threadIdx.x; i < m; i += gthreads<NTG>()) {
+      if (i > cc) A[i + cc * lda] *= sc;
+      else A[i + cc * lda] = s_beta[cc];
+    }
+  }
+  gsync<NTG>();
 }
 
 // G = V_p^T V_p (32 x 32) on the tensor cores; warp w < 16 computes one 8x8 block.
@@ -553,11 +835,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
     const int j0 = p * kP, nbp = min(kP, n - j0);
     double* T = Tbase + (args.mode == kGeqrfOrtho ? p * kP * kLdT : 0);
     HQR_MARK(2 + 4 * p);
-    panel_factor<MR, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr, Tscr + 64, G,
-                     Tscr + 128);
+    if constexpr (MR <= 6) panel_factor_q<MR * 4, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
+    else panel_factor_wide<MR, NT / 32, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
     HQR_MARK(3 + 4 * p);
-    panel_gram<0>(A, lda, m, j0, nbp, G);
-    __syncthreads();
     form_t<0>(T, Tscr, G, s_tau, j0, nbp);
     if (args.mode == kGeqrfFactor) {
       double* tout = S.t + (size_t)b * S.t_stride + (size_t)p * kP * kP;
@@ -864,16 +1144,17 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     for (int p = 0; p < npanel; ++p) {
       const int j0 = p * kP, nbp = min(kP, n - j0);
       if (p >= 2) mbar_wait(&s_ready[16 + p - 2], 0);   // panels <= p-2 applied to my columns by group Y
+      if (threadIdx.x == 0) FUSED_MARK(21 + 2 * p);
       if (p >= 1) {                                      // look-ahead: apply panel p-1 to panel p's columns
         const int jp = j0 - kP;
         block_reflector_apply<256>(A, lda, round_up(m, 8), jp, kP, tglob + (size_t)(p - 1) * kP * kP, true, j0,
                                    j0 + nbp, kP);
         gsync<256>();
       }
-      panel_factor<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), Tscr,
-                            Tscr + 64, G, Tscr + 128);
-      panel_gram<256>(A, lda, m, j0, nbp, G);
-      gsync<256>();
+      if (threadIdx.x == 0) FUSED_MARK(22 + 2 * p);
+      if constexpr (MR <= 6) panel_factor_q<MR * 4, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
+      else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
+      if (threadIdx.x == 0) FUSED_MARK(42 + p);
       form_t<256>(T, Tscr, G, s_tau, j0, nbp);
       for (int e = threadIdx.x; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
       __threadfence_block();

@@ -94,3 +94,42 @@ def test_probe_qr_zero_block():
     vt, r, tau, t, rinv, st = probe_qr([np.zeros((8, 20))], 20)
     assert st[0] == 1          # sigma_max == 0 -> rank deficient (linalg.py:73)
     assert not np.any(tau)     # dlarfg: zero column -> tau = 0, H = I
+
+
+def basis_qr(blocks, r):
+    rows = [b.shape[0] for b in blocks]
+    nr = max(rows)
+    begins = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    sq = np.concatenate([[0], np.cumsum(np.array(rows) ** 2)]).astype(np.int64)
+    dev = torch.device("cuda")
+    bb = torch.from_numpy(np.concatenate(blocks)).to(dev)
+    q = torch.zeros_like(bb)
+    rb, so = torch.from_numpy(begins).to(dev), torch.from_numpy(sq).to(dev)
+    sz = ctypes.c_size_t()
+    _native.check(_native.lib().hbs_basis_qr_scratch_bytes(len(blocks), nr, r, ctypes.byref(sz)), "scratch")
+    scratch = torch.empty(max(sz.value // 8, 1), dtype=torch.float64, device=dev)
+    rc = _native.lib().hbs_basis_qr(len(blocks), rb.data_ptr(), so.data_ptr(), nr, r, bb.data_ptr(), q.data_ptr(),
+                                    scratch.data_ptr() if sz.value else 0, torch.cuda.current_stream().cuda_stream)
+    _native.check(rc, "hbs_basis_qr")
+    torch.cuda.synchronize()
+    out, qh = [], q.cpu().numpy()
+    for j in range(len(blocks)):
+        out.append(qh[begins[j]:begins[j + 1]])
+    return out
+
+
+@pytest.mark.parametrize("rows,r", [(32, 16), (21, 8), (128, 64), (64, 32), (48, 24), (144, 72), (30, 15), (40, 40)])
+def test_basis_qr_matches_lapack(rows, r):
+    """col() building block: reduced QR with explicit Q (linalg.py:35-49)."""
+    rng = np.random.default_rng(rows * 100 + r)
+    blocks = [rng.standard_normal((rows, r)) for _ in range(3)]
+    blocks.append(np.zeros((rows, r)))                      # zero block: Q = leading identity columns
+    low = rng.standard_normal((rows, 2)) @ rng.standard_normal((2, r))
+    blocks.append(low)                                      # rank-deficient block (oversampled case)
+    qs = basis_qr(blocks, r)
+    for b, q in zip(blocks, qs):
+        q_ref = np.linalg.qr(b)[0][:, :r]
+        assert np.linalg.norm(q.T @ q - np.eye(r)) <= 1e-12 * r
+        if np.linalg.matrix_rank(b) == r:
+            assert np.abs(q - q_ref).max() <= 1e-11      # same reflectors => same Q (LAPACK signs)
+        assert np.linalg.norm(b - q @ (q.T @ b)) <= 1e-12 * max(1.0, np.linalg.norm(b))

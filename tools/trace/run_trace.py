@@ -28,6 +28,10 @@ f = t[128:128 + 48]
 print("FUSED (cycles from start):", {"P panel ready": [f[1 + 2 * p] - f[0] for p in range(4)],
       "P trailing done": [f[2 + 2 * p] - f[0] for p in range(4)], "P rinv done": f[20] - f[0],
       "Y panel done": [f[30 + p] - f[0] for p in range(4)], "Y solve start": f[40] - f[0], "Y end": f[41] - f[0]})
+print("P per panel: start", [f[21 + 2 * p] - f[0] for p in range(4)], "pre-update done", [f[22 + 2 * p] - f[0] for p in range(4)],
+      "factor done", [f[42 + p] - f[0] for p in range(4)])
+sm = t[200:208]
+print("STEP(j=6, panel 1, publisher): wait", sm[1]-sm[0], "loads+dots", sm[2]-sm[1], "reduce", sm[3]-sm[2], "updates until pub", sm[4]-sm[3], "norm+store", sm[5]-sm[4], "reflector", sm[6]-sm[5], "arrive", sm[7]-sm[6])
 print("load", t[1] - t[0])
 for p in range(4):
     a = 2 + 4 * p
