@@ -579,7 +579,10 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
       for (int jl = 0; jl < 8; ++jl) {
         const int j = 8 * kb + jl, jj = j0 + j;
         if (j >= nbp) break;
+        const bool tr = (j == 6) && own && (q == 7) && li == 0;
+        if (tr) STEP_MARK(0);
         mbar_wait(&bar[j], parity);
+        if (tr) STEP_MARK(1);
         const double tau = s_tau[jj], scale = s_scale[jj];
         double pv[MR8];
 #pragma unroll
@@ -607,6 +610,7 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
           for (int k = 0; k < MR8; ++k)
             if (li + 8 * k > j + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
         }
+        if (tr) STEP_MARK(2);
         double d = (d0 + d1) + (d2 + d3);
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {
@@ -614,6 +618,7 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
           sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
           spp += __shfl_xor_sync(0xffffffffu, spp, o);
         }
+        if (tr) STEP_MARK(3);
         if (own && c < jj) {            // retired reflector: compact-WY dot
           if (li == 0) G[q * kLdT + j] = s_scale[c] * (r + scale * d);
         } else if (own && c > jj) {
@@ -622,6 +627,7 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
           for (int k = 0; k < MR8; ++k) x[k] = fma(-gs, pv[k], x[k]);
           if (li == jl) x[kb] -= f;
           if (pub) {
+            if (tr) STEP_MARK(4);
             const double sxp = d - pn * xn_old;
             double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
             double p = 0.0;
@@ -639,11 +645,14 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
               if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
             const double alpha = (jl == 7) ? __shfl_sync(0x000000ffu << gbase, x[kb < 3 ? kb + 1 : kb], gbase)
                                            : __shfl_sync(0x000000ffu << gbase, x[kb], gbase | (jl + 1));
+            if (tr) STEP_MARK(5);
             __syncwarp(0x000000ffu << gbase);
             if (li == 0) {
               const Reflector h = make_reflector(alpha, nrm);
               s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+              if (tr) STEP_MARK(6);
               mbar_arrive(&bar[j + 1]);
+              if (tr) STEP_MARK(7);
             }
           }
         }
