@@ -134,6 +134,26 @@ int hbs_apply(int depth, int r, int64_t n, int64_t c,
               const double* root, const double* q, double* out, int transpose,
               void* workspace, size_t workspace_bytes, void* stream);
 
+/* The three sweeps of hbs_apply, exposed for the subtree-partitioned sampler
+ * (one process per GPU: local upward pass, all-gather of qhat at the
+ * partition level, replicated top, local downward pass).  Per-level host
+ * arrays are indexed by level number: nbox[l], row_begin[l], sq_off[l]
+ * (device), basis[l] / d[l] (device), qhat[l] / uhat[l] (device, box b's
+ * r x c block at b*r*c).
+ *   up:   qhat[l] = basis_l^T (l == level_hi ? q : qhat[l+1]),  l = level_hi .. level_lo
+ *   root: uhat1 = root^(T) qhat1                                  (2r x c)
+ *   down: (l == level_hi ? out : uhat[l+1]) = basis_l uhat[l] + d_l^(T) (l == level_hi ? q : qhat[l+1]),
+ *         l = level_lo .. level_hi; max_rows_hi = largest box at level_hi. */
+int hbs_apply_up(int level_hi, int level_lo, int r, int64_t c, const int64_t* nbox,
+                 const int64_t* const* row_begin, const int64_t* const* sq_off, const double* const* basis,
+                 const double* q, double* const* qhat, void* stream);
+int hbs_apply_root(int r, int64_t c, const double* root, int transpose, const double* qhat1, double* uhat1,
+                   void* stream);
+int hbs_apply_down(int level_lo, int level_hi, int r, int64_t c, const int64_t* nbox,
+                   const int64_t* const* row_begin, const int64_t* const* sq_off, int max_rows_hi,
+                   const double* const* basis, const double* const* d, int transpose_d, double* const* uhat,
+                   const double* const* qhat, const double* q, double* out, void* stream);
+
 /* Dense sampler out = A q or A^T q for an explicit n x n row-major A
  * (operators.py:213-218). */
 int hbs_dense_apply(int64_t n, int64_t c, const double* a, const double* q, double* out,

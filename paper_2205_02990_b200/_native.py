@@ -43,6 +43,9 @@ SIGNATURES = {
     "hbs_compress_root": ([_P, _P, _I, _I, _D, _P, _P, _P, _P, _SZ, _P, _P], _I),
     "hbs_apply_workspace_bytes": ([_I, _I, _I64, ctypes.POINTER(_SZ)], _I),
     "hbs_apply": ([_I, _I, _I64, _I64, _PP, _PP, _PP, _PP, _PP, _P, _P, _P, _I, _P, _SZ, _P], _I),
+    "hbs_apply_up": ([_I, _I, _I, _I64, _P, _PP, _PP, _PP, _P, _PP, _P], _I),
+    "hbs_apply_root": ([_I, _I64, _P, _I, _P, _P, _P], _I),
+    "hbs_apply_down": ([_I, _I, _I, _I64, _P, _PP, _PP, _I, _PP, _PP, _I, _PP, _PP, _P, _P, _P], _I),
     "hbs_dense_apply": ([_I64, _I64, _P, _P, _P, _I, _P], _I),
     "hbs_fill_log_kernel": ([_I64, _I64, _I64, _P, _P], _I),
 }

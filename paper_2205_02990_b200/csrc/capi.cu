@@ -387,6 +387,56 @@ int hbs_compress_root(const int64_t* row_begin, const int64_t* sq_off, int rows,
 }
 
 // ------------------------------------------------------------------ samplers
+int hbs_apply_up(int level_hi, int level_lo, int r, int64_t c, const int64_t* nbox,
+                 const int64_t* const* row_begin, const int64_t* const* sq_off, const double* const* basis,
+                 const double* q, double* const* qhat, void* stream) {
+  if (level_lo < 0 || level_hi < level_lo || r < 1 || c < 1 || c > (1 << 30)) return HBS_ERR_DIMENSION;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cc = (int)c;
+  const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
+  for (int l = level_hi; l >= level_lo; --l) {
+    const LevelGeo geo{row_begin[l], sq_off[l], nbox[l]};
+    const double* src = (l == level_hi) ? q : qhat[l + 1];
+    HBS_TRY(gemm(geo, dfix(r), dfix(cc), drows(), r, cc, op(basis[l], r, 0, 0, r, false, true),
+                 op(src, cc, 0, 0, cc, false, false), qhat[l], 0, (int64_t)r * cc, 0, cc, false, 1.0, 0.0, none, st));
+  }
+  return HBS_OK;
+}
+
+int hbs_apply_root(int r, int64_t c, const double* root, int transpose, const double* qhat1, double* uhat1,
+                   void* stream) {
+  if (r < 1 || c < 1 || c > (1 << 30)) return HBS_ERR_DIMENSION;
+  const LevelGeo geo{nullptr, nullptr, 1};
+  const int cc = (int)c;
+  return gemm(geo, dfix(2 * r), dfix(cc), dfix(2 * r), 2 * r, cc, op(root, 0, 0, 0, 2 * r, false, transpose != 0),
+              op(qhat1, 0, 0, 0, cc, false, false), uhat1, 0, 0, 0, cc, false, 1.0, 0.0,
+              op(nullptr, 0, 0, 0, 0, false, false), static_cast<cudaStream_t>(stream));
+}
+
+int hbs_apply_down(int level_lo, int level_hi, int r, int64_t c, const int64_t* nbox,
+                   const int64_t* const* row_begin, const int64_t* const* sq_off, int max_rows_hi,
+                   const double* const* basis, const double* const* d, int transpose_d, double* const* uhat,
+                   const double* const* qhat, const double* q, double* out, void* stream) {
+  if (level_lo < 0 || level_hi < level_lo || r < 1 || c < 1 || c > (1 << 30) || max_rows_hi < 1)
+    return HBS_ERR_DIMENSION;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cc = (int)c;
+  const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
+  for (int l = level_lo; l <= level_hi; ++l) {
+    const LevelGeo geo{row_begin[l], sq_off[l], nbox[l]};
+    const bool last = (l == level_hi);
+    double* dst = last ? out : uhat[l + 1];
+    const double* rhs = last ? q : qhat[l + 1];
+    const int mmax = last ? max_rows_hi : 2 * r;
+    HBS_TRY(gemm(geo, drows(), dfix(cc), dfix(r), mmax, cc, op(basis[l], r, 0, 0, r, false, false),
+                 op(uhat[l], 0, (int64_t)r * cc, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 0.0, none, st));
+    HBS_TRY(gemm(geo, drows(), dfix(cc), drows(), mmax, cc, op(d[l], 0, 0, 1, 0, true, transpose_d != 0),
+                 op(rhs, cc, 0, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 1.0,
+                 op(dst, cc, 0, 0, cc, false, false), st));
+  }
+  return HBS_OK;
+}
+
 int hbs_apply_workspace_bytes(int depth, int r, int64_t c, size_t* bytes) {
   if (depth < 1 || r < 1 || c < 1 || !bytes) return HBS_ERR_DIMENSION;
   // qhat and uhat for every level: sum_l 2^l r c, twice.
@@ -399,54 +449,26 @@ int hbs_apply(int depth, int r, int64_t n, int64_t c, const int64_t* const* row_
               const int64_t* const* sq_off, const double* const* u, const double* const* v,
               const double* const* d, const double* root, const double* q, double* out, int transpose,
               void* workspace, size_t workspace_bytes, void* stream) {
-  if (depth < 1 || r < 1 || n < 2 || c < 1) return HBS_ERR_DIMENSION;
+  if (depth < 1 || depth > 60 || r < 1 || n < 2 || c < 1) return HBS_ERR_DIMENSION;
   if (c > (1 << 30)) return HBS_ERR_UNSUPPORTED;
   size_t need;
   hbs_apply_workspace_bytes(depth, r, c, &need);
   if (need > workspace_bytes) return HBS_ERR_WORKSPACE;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int cc = (int)c;
-  // level buffers: qhat[l], uhat[l] hold 2^l * r rows of c columns
   double* base = static_cast<double*>(workspace);
   double* qhat[64];
   double* uhat[64];
+  int64_t nbox[64];
   size_t off = 0;
   for (int l = 1; l <= depth; ++l) { qhat[l] = base + off; off += ((size_t)1 << l) * r * c; }
   for (int l = 1; l <= depth; ++l) { uhat[l] = base + off; off += ((size_t)1 << l) * r * c; }
+  for (int l = 0; l <= depth; ++l) nbox[l] = (int64_t)1 << l;
+  const int leaf_max = (int)((n + ((int64_t)1 << depth) - 1) >> depth);
   const double* const* up = transpose ? u : v;
   const double* const* down = transpose ? v : u;
-  const BOperand none = op(nullptr, 0, 0, 0, 0, false, false);
-  // leaf rows: max rows of the leaf level
-  const int leaf_max = (int)((n + ((int64_t)1 << depth) - 1) >> depth);
-  // upward pass (factorization.py:111-119)
-  for (int l = depth; l >= 1; --l) {
-    const LevelGeo geo{row_begin[l], sq_off[l], (int64_t)1 << l};
-    const double* src = (l == depth) ? q : qhat[l + 1];
-    HBS_TRY(gemm(geo, dfix(r), dfix(cc), drows(), r, cc, op(up[l], r, 0, 0, r, false, true),
-                 op(src, cc, 0, 0, cc, false, false), qhat[l], 0, (int64_t)r * cc, 0, cc, false, 1.0, 0.0,
-                 none, st));
-  }
-  // root (factorization.py:121-125): uhat[1] = D_root^(T) qhat[1]
-  {
-    const LevelGeo geo{nullptr, nullptr, 1};
-    HBS_TRY(gemm(geo, dfix(2 * r), dfix(cc), dfix(2 * r), 2 * r, cc, op(root, 0, 0, 0, 2 * r, false, transpose != 0),
-                 op(qhat[1], 0, 0, 0, cc, false, false), uhat[1], 0, 0, 0, cc, false, 1.0, 0.0, none, st));
-  }
-  // downward pass (factorization.py:127-142)
-  for (int l = 1; l <= depth; ++l) {
-    const LevelGeo geo{row_begin[l], sq_off[l], (int64_t)1 << l};
-    const bool leaf = (l == depth);
-    double* dst = leaf ? out : uhat[l + 1];
-    const double* rhs = leaf ? q : qhat[l + 1];
-    const int mmax = leaf ? leaf_max : 2 * r;
-    HBS_TRY(gemm(geo, drows(), dfix(cc), dfix(r), mmax, cc, op(down[l], r, 0, 0, r, false, false),
-                 op(uhat[l], 0, (int64_t)r * cc, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 0.0,
-                 none, st));
-    HBS_TRY(gemm(geo, drows(), dfix(cc), drows(), mmax, cc, op(d[l], 0, 0, 1, 0, true, transpose != 0),
-                 op(rhs, cc, 0, 0, cc, false, false), dst, cc, 0, 0, cc, false, 1.0, 1.0,
-                 op(dst, cc, 0, 0, cc, false, false), st));
-  }
-  return HBS_OK;
+  HBS_TRY(hbs_apply_up(depth, 1, r, c, nbox, row_begin, sq_off, up, q, qhat, stream));
+  HBS_TRY(hbs_apply_root(r, c, root, transpose, qhat[1], uhat[1], stream));
+  return hbs_apply_down(1, depth, r, c, nbox, row_begin, sq_off, leaf_max, down, d, transpose, uhat, qhat, q, out,
+                        stream);
 }
 
 int hbs_dense_apply(int64_t n, int64_t c, const double* a, const double* q, double* out, int transpose,

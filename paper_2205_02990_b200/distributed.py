@@ -18,12 +18,16 @@ exercise this host logic with the gloo backend.
 
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native
 from .compress import CompressionConfig, CompressPlan, _check_configuration, raise_ill_conditioned
 from .errors import ConfigurationError
+from .factorization import LevelGeometry
 from .tree import ClusterTree
 
 
@@ -40,7 +44,7 @@ class SubtreePartition:
         top = tree.level_begin(lg)
         self.begin, self.end = int(top[rank]), int(top[rank + 1])
         self.local_specs = []
-        for level in range(tree.depth, lg - 1, -1):
+        for level in range(tree.depth, max(lg, 1) - 1, -1):
             nb = 1 << (level - lg)
             first = rank * nb
             if level == tree.depth:
@@ -215,3 +219,173 @@ def compress_partitioned_on_one_device(samples, tree: ClusterTree, config: Compr
     blocks.update(DistributedFactorization(part, top, None).host_blocks(top))
     root = top.root
     return blocks, (root.cpu().numpy() if isinstance(root, torch.Tensor) else np.asarray(root))
+
+
+# ---------------------------------------------------------------------------
+# Distributed telescoping operator (the HBS sampler of SURVEY 8(e)) and a
+# preallocated distributed compressor for repeated runs (bench.py).
+# ---------------------------------------------------------------------------
+
+def _level_arrays(geo: dict, blocks: dict, lo: int, hi: int, which: int):
+    n = hi + 1
+    nbox = (ctypes.c_int64 * n)()
+    rb = _native.ptr_array([0] * n)
+    sq = _native.ptr_array([0] * n)
+    bp = _native.ptr_array([0] * n)
+    for lv in range(lo, hi + 1):
+        nbox[lv] = geo[lv].nbox
+        rb[lv] = geo[lv].row_begin.data_ptr()
+        sq[lv] = geo[lv].sq_off.data_ptr()
+        bp[lv] = blocks[lv][which].data_ptr()
+    return nbox, rb, sq, bp
+
+
+class DistributedOperator:
+    """A telescoping factorization split by subtree: this rank's levels
+    lg..L (its boxes only) plus the replicated top levels 1..lg-1 and root.
+    `apply` is the distributed sampler: local upward pass, one all-gather of
+    qhat at level lg (r x c per rank), the top levels on every rank, then the
+    local downward pass (factorization.py:89-143 split at level lg)."""
+
+    def __init__(self, partition: SubtreePartition, local_blocks: dict, local_geo: dict, top_blocks: dict,
+                 top_geo: dict, root, group=None):
+        self.part, self.group = partition, group
+        self.local_blocks, self.local_geo = local_blocks, local_geo
+        self.top_blocks, self.top_geo, self.root = top_blocks, top_geo, root
+        self.device = root.device
+
+    # the three phases of `apply`, exposed so that a single-device test can
+    # emulate several ranks (concatenation in place of the all-gather)
+    def up_local(self, q, transpose=False):
+        part, r = self.part, self.part.r
+        L, lo = part.tree.depth, max(part.lg, 1)
+        c = q.shape[1]
+        f64 = dict(dtype=torch.float64, device=self.device)
+        qhat = {lv: torch.empty(self.local_geo[lv].nbox * r, c, **f64) for lv in range(lo, L + 1)}
+        nbox, rb, sq, bp = _level_arrays(self.local_geo, self.local_blocks, lo, L, 0 if transpose else 1)
+        qp = _native.ptr_array([0] * (L + 1))
+        for lv in range(lo, L + 1):
+            qp[lv] = qhat[lv].data_ptr()
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(_native.lib().hbs_apply_up(L, lo, r, c, nbox, rb, sq, bp, q.data_ptr(), qp, st),
+                      "hbs_apply_up")
+        return qhat
+
+    def top(self, qtop, transpose=False):
+        """qtop: level-lg qhat of all ranks ((world r) x c, rank order) -> uhat at level lg, all ranks."""
+        part, r, lg = self.part, self.part.r, self.part.lg
+        c = qtop.shape[1]
+        lib, st = _native.lib(), torch.cuda.current_stream(self.device).cuda_stream
+        f64 = dict(dtype=torch.float64, device=self.device)
+        tq = {lv: torch.empty((1 << lv) * r, c, **f64) for lv in range(1, lg)}
+        tu = {lv: torch.empty((1 << lv) * r, c, **f64) for lv in range(1, lg + 1)}
+        tqp, tup = _native.ptr_array([0] * (lg + 1)), _native.ptr_array([0] * (lg + 1))
+        for lv in range(1, lg):
+            tqp[lv] = tq[lv].data_ptr()
+        for lv in range(1, lg + 1):
+            tup[lv] = tu[lv].data_ptr()
+        q1 = qtop
+        if lg >= 2:
+            tn, trb, tsq, tbp = _level_arrays(self.top_geo, self.top_blocks, 1, lg - 1, 0 if transpose else 1)
+            _native.check(lib.hbs_apply_up(lg - 1, 1, r, c, tn, trb, tsq, tbp, qtop.data_ptr(), tqp, st),
+                          "hbs_apply_up(top)")
+            q1 = tq[1]
+        _native.check(lib.hbs_apply_root(r, c, self.root.data_ptr(), 1 if transpose else 0, q1.data_ptr(),
+                                         tu[1].data_ptr(), st), "hbs_apply_root")
+        if lg >= 2:
+            tn, trb, tsq, tbp = _level_arrays(self.top_geo, self.top_blocks, 1, lg - 1, 1 if transpose else 0)
+            _, _, _, tdp = _level_arrays(self.top_geo, self.top_blocks, 1, lg - 1, 2)
+            _native.check(lib.hbs_apply_down(1, lg - 1, r, c, tn, trb, tsq, 2 * r, tbp, tdp, 1 if transpose else 0,
+                                             tup, tqp, qtop.data_ptr(), tu[lg].data_ptr(), st), "hbs_apply_down(top)")
+        return tu[lg]
+
+    def down_local(self, q, qhat, uhat_lg, transpose=False):
+        part, r = self.part, self.part.r
+        L, lo = part.tree.depth, max(part.lg, 1)
+        c = q.shape[1]
+        f64 = dict(dtype=torch.float64, device=self.device)
+        uhat = {lv: torch.empty(self.local_geo[lv].nbox * r, c, **f64) for lv in range(lo + 1, L + 1)}
+        uhat[lo] = uhat_lg.contiguous()
+        up_, qp = _native.ptr_array([0] * (L + 1)), _native.ptr_array([0] * (L + 1))
+        for lv in range(lo, L + 1):
+            up_[lv], qp[lv] = uhat[lv].data_ptr(), qhat[lv].data_ptr()
+        out = torch.empty_like(q)
+        nbox, rb, sq, bp = _level_arrays(self.local_geo, self.local_blocks, lo, L, 1 if transpose else 0)
+        _, _, _, dp = _level_arrays(self.local_geo, self.local_blocks, lo, L, 2)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(_native.lib().hbs_apply_down(lo, L, r, c, nbox, rb, sq, self.local_geo[L].max_rows, bp, dp,
+                                                   1 if transpose else 0, up_, qp, q.data_ptr(), out.data_ptr(), st),
+                      "hbs_apply_down")
+        return out
+
+    def apply(self, q, transpose=False):
+        """Distributed A q (A^T q) for this rank's rows of q."""
+        part, r = self.part, self.part.r
+        q = q.contiguous()
+        qhat = self.up_local(q, transpose)
+        if part.world == 1:
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            u1 = torch.empty(2 * r, q.shape[1], dtype=torch.float64, device=self.device)
+            _native.check(_native.lib().hbs_apply_root(r, q.shape[1], self.root.data_ptr(), 1 if transpose else 0,
+                                                       qhat[1].data_ptr(), u1.data_ptr(), st), "hbs_apply_root")
+            return self.down_local(q, qhat, u1, transpose)
+        lg = part.lg
+        qtop = torch.empty(part.world * r * q.shape[1], dtype=torch.float64, device=self.device)
+        dist.all_gather_into_tensor(qtop, qhat[lg].reshape(-1), group=self.group)
+        ulg = self.top(qtop.reshape(part.world * r, q.shape[1]), transpose)
+        return self.down_local(q, qhat, ulg[part.rank * r:(part.rank + 1) * r], transpose)
+
+
+class DistributedCompressor:
+    """Preallocated subtree-partitioned compressor (CUDA): `run` enqueues the
+    local sweep, the all-gather of lifted halves and the replicated top sweep;
+    `operator()` wraps the result as a DistributedOperator."""
+
+    def __init__(self, tree: ClusterTree, partition: SubtreePartition, s: int, tol: float = 1e-10, device=None,
+                 group=None):
+        self.part, self.s, self.group = partition, s, group
+        r = partition.r
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.local = CompressPlan(tree, s, r, tol, device=self.device, specs=partition.local_specs,
+                                  with_root=(partition.world == 1))
+        self.top = None
+        if partition.world > 1:
+            self.top = CompressPlan(tree, s, r, tol, device=self.device, specs=partition.top_specs, with_root=True)
+            self.gathered = torch.empty(partition.world * 4 * r * s, dtype=torch.float64, device=self.device)
+            self.top_quad = [torch.empty(partition.world * r, s, dtype=torch.float64, device=self.device)
+                             for _ in range(4)]
+            self.half = torch.empty(4, r, s, dtype=torch.float64, device=self.device)
+
+    def run(self, omega, psi, y, z):
+        self.local.run(omega, psi, y, z)
+        if self.top is None:
+            return
+        w, r, s = self.part.world, self.part.r, self.s
+        for i, m in enumerate(self.local.top_quad):
+            self.half[i].copy_(m.reshape(r, s))
+        dist.all_gather_into_tensor(self.gathered, self.half.reshape(-1), group=self.group)
+        g = self.gathered.reshape(w, 4, r, s)
+        for i in range(4):
+            self.top_quad[i].copy_(g[:, i].reshape(w * r, s))
+        if self.top.specs:
+            self.top.run(*self.top_quad)
+        else:
+            self.top.top_quad = tuple(self.top_quad)
+            self.top.run_root(self.top_quad[0], self.top_quad[2])
+
+    def raise_for_status(self):
+        fail = self.local.first_failure()
+        if self.top is not None:
+            fail = _agree_on_failure(fail, self.group)
+            if fail is None:
+                fail = self.top.first_failure()
+        if fail is not None:
+            raise_ill_conditioned(*fail, self.local.tol)
+
+    def operator(self) -> DistributedOperator:
+        top_blocks = {} if self.top is None else {lv: self.top.levels[lv] for lv, _, _ in self.top.specs}
+        top_geo = {} if self.top is None else {lv: self.top.geometry[lv] for lv, _, _ in self.top.specs}
+        root = self.local.root if self.top is None else self.top.root
+        return DistributedOperator(self.part, {lv: self.local.levels[lv] for lv, _, _ in self.part.local_specs},
+                                   {lv: self.local.geometry[lv] for lv, _, _ in self.part.local_specs},
+                                   top_blocks, top_geo, root, self.group)

@@ -80,3 +80,60 @@ def device_samples(f: HbsFactorization, s: int, seed: int = 0):
     om = torch.randn(f.n, s, generator=gen, dtype=torch.float64, device=f.device)
     ps = torch.randn(f.n, s, generator=gen, dtype=torch.float64, device=f.device)
     return om, ps, apply_matrix(f, om), apply_matrix(f, ps, transpose=True)
+
+
+def _gen_level(gen, begins, k, leaf, decay, dev):
+    """(U, V, D) packed for one level with row starts `begins` (numpy)."""
+    sizes = np.diff(begins)
+    nbox = sizes.size
+    if not leaf:
+        u = _orthonormal(gen, nbox, 2 * k, k, dev).reshape(-1, k)
+        v = _orthonormal(gen, nbox, 2 * k, k, dev).reshape(-1, k)
+        d = torch.zeros(nbox, 2 * k, 2 * k, dtype=torch.float64, device=dev)
+        d[:, :k, k:] = _coupling(gen, nbox, k, decay, dev)
+        d[:, k:, :k] = _coupling(gen, nbox, k, decay, dev)
+        return u.contiguous(), v.contiguous(), d.reshape(-1).contiguous()
+    us, vs, ds = [], [], []
+    for m in np.unique(sizes):
+        pass
+    if (sizes == sizes[0]).all():
+        m = int(sizes[0])
+        u = _orthonormal(gen, nbox, m, k, dev).reshape(-1, k)
+        v = _orthonormal(gen, nbox, m, k, dev).reshape(-1, k)
+        d = torch.randn(nbox, m, m, generator=gen, dtype=torch.float64, device=dev) / math.sqrt(m)
+        d += torch.eye(m, dtype=torch.float64, device=dev)
+        return u.contiguous(), v.contiguous(), d.reshape(-1).contiguous()
+    for m in sizes:
+        m = int(m)
+        us.append(_orthonormal(gen, 1, m, k, dev)[0])
+        vs.append(_orthonormal(gen, 1, m, k, dev)[0])
+        dd = torch.randn(m, m, generator=gen, dtype=torch.float64, device=dev) / math.sqrt(m)
+        ds.append((dd + torch.eye(m, dtype=torch.float64, device=dev)).reshape(-1))
+    return torch.cat(us), torch.cat(vs), torch.cat(ds)
+
+
+def partitioned_generator(partition, k, seed=0, decay=None, device=None, group=None):
+    """Exact-rank synthetic operator split by subtree (distributed.SubtreePartition):
+    the rank's local levels from seed (seed, rank) and the replicated top
+    levels + root from a seed shared by all ranks.  Returns a
+    distributed.DistributedOperator (the multi-GPU sampler)."""
+    from .distributed import DistributedOperator
+    from .factorization import LevelGeometry
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    tree = partition.tree
+    gl = torch.Generator(device=dev)
+    gl.manual_seed(1_000_000 * (seed + 1) + partition.rank)
+    local_blocks, local_geo = {}, {}
+    for level, begins, _ in partition.local_specs:
+        local_geo[level] = LevelGeometry(begins, dev)
+        local_blocks[level] = _gen_level(gl, begins, k, level == tree.depth, decay, dev)
+    gt = torch.Generator(device=dev)
+    gt.manual_seed(seed)
+    top_blocks, top_geo = {}, {}
+    for level, begins, _ in partition.top_specs:
+        top_geo[level] = LevelGeometry(begins, dev)
+        top_blocks[level] = _gen_level(gt, begins, k, False, decay, dev)
+    root = torch.zeros(2 * k, 2 * k, dtype=torch.float64, device=dev)
+    root[:k, k:] = _coupling(gt, 1, k, decay, dev)[0]
+    root[k:, :k] = _coupling(gt, 1, k, decay, dev)[0]
+    return DistributedOperator(partition, local_blocks, local_geo, top_blocks, top_geo, root, group)

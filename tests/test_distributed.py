@@ -140,6 +140,6 @@ def test_partition_geometry():
             spans.append((p.begin, p.end))
             leaf = p.local_specs[0]
             assert leaf[0] == tree.depth and leaf[1][0] == 0 and leaf[1][-1] == p.rows
-            assert [s[0] for s in p.local_specs] == list(range(tree.depth, p.lg - 1, -1))
+            assert [s[0] for s in p.local_specs] == list(range(tree.depth, max(p.lg, 1) - 1, -1))
         assert spans[0][0] == 0 and spans[-1][1] == 333
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
