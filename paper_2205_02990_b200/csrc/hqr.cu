@@ -1192,6 +1192,19 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   const int yw = warp - 8;
   const double* y0 = S.y + S.y_c_rb * rb;
   double* yq = S.yq + (size_t)b * S.yq_stride;
+  // 16-byte vector accesses only when every row start is 16-byte aligned
+  const bool vec2 = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(y0) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(yq) & 15) == 0);
+  // (with odd s the pair (col, col+1) may end one past the row: the second
+  // element is then neither read nor written)
+  auto ld2 = [&](const double* p, bool second) -> double2 {
+    if (vec2) return __ldcg(reinterpret_cast<const double2*>(p));
+    return make_double2(__ldcg(p), second ? __ldcg(p + 1) : 0.0);
+  };
+  auto st2 = [&](double* p, double2 v, bool second) {
+    if (vec2) *reinterpret_cast<double2*>(p) = v;
+    else { p[0] = v.x; if (second) p[1] = v.y; }
+  };
   const int spad = round_up(s, 8);
   const int ngroups = (nb + 7) >> 3;
   for (int p = 0; p < npanel; ++p) {
@@ -1256,14 +1269,14 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       // C-fragment loads issued 4 column blocks ahead
       if (p == 0) {
         for (int c = 2 * t; c < kb; c += 8)
-          if (rok) *reinterpret_cast<double2*>(drow + c) = __ldcg(reinterpret_cast<const double2*>(srow + c));
+          if (rok) st2(drow + c, ld2(srow + c, c + 1 < kb), c + 1 < kb);
       }
       for (int nc = kb; nc < spad; nc += 32) {
         double2 cv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int col = nc + 8 * u + 2 * t;
-          cv[u] = (rok && col < s) ? __ldcg(reinterpret_cast<const double2*>(srow + col)) : make_double2(0.0, 0.0);
+          cv[u] = (rok && col < s) ? ld2(srow + col, col + 1 < s) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1284,7 +1297,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int col = nc + 8 * u + 2 * t;
-          if (rok && col < s && nc + 8 * u < spad) *reinterpret_cast<double2*>(drow + col) = cv[u];
+          if (rok && col < s && nc + 8 * u < spad) st2(drow + col, cv[u], col + 1 < s);
         }
       }
       __syncwarp();
