@@ -36,6 +36,10 @@ HBS_DEV void dmma8x8x4(double& c0, double& c1, double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Warp index broadcast from lane 0: provably warp-uniform to the compiler, so
+// branches on it do not force WARPSYNC.COLLECTIVE around later shuffles.
+HBS_DEV int uniform_warp(int w) { return __shfl_sync(0xffffffffu, w, 0); }
+
 HBS_DEV double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -81,6 +85,15 @@ HBS_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+
+// Warp-uniform wait: one lane spins (acquire), then __syncwarp re-converges the
+// warp and orders the other lanes' later reads after the acquire.  Waiting in
+// every lane leaves the compiler unable to prove convergence afterwards, and
+// it then emits WARPSYNC.COLLECTIVE sequences around every later shuffle.
+HBS_DEV void mbar_wait_warp(uint64_t* bar, unsigned parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // cp.async (LDGSTS) helpers: 8-byte element copies with zero fill.

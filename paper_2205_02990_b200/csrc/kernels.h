@@ -54,10 +54,6 @@ struct GeqrfArgs {
   int use_smem;
 };
 
-size_t geqrf_smem_bytes(int m_max, int n_max, int mode);
-size_t geqrf_scratch_doubles(int m_max, int n_max, int64_t nbox);
-int launch_geqrf(GeqrfArgs args, int nsides, cudaStream_t stream);
-
 // Blocked Householder (hqr.cu): kFactor also emits the per-panel T and R
 // diagonal-block inverses (PanelSide layout) through GeqrfSide::t / rinv.
 size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix);
@@ -86,24 +82,6 @@ struct FusedArgs {
 };
 bool fused_fits(int s, int n_max);
 int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream);
-
-// ---------------------------------------------------------------- panel factors
-// Per (box, side, panel): compact-WY T block (dlarft, forward/columnwise) of
-// the reflectors j0..j0+NB-1 and the inverse of R's diagonal block.
-struct PanelSide {
-  const double* vt; int64_t vt_stride; int ldvt;
-  const double* r; int64_t r_stride; int ldr;
-  const double* tau; int64_t tau_stride;
-  double* t; int64_t t_stride;        // npanel * NB * NB per box, row-major NB x NB blocks
-  double* rinv; int64_t rinv_stride;  // same shape
-};
-struct PanelArgs {
-  LevelGeo geo;
-  PanelSide side[2];
-  int m;       // reflector length (s)
-  int n_fixed, n_is_rows, n_max;
-};
-int launch_panel_factors(PanelArgs args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- apply Q + solve
 // Per (row tile, box, side): Yt <- Y_tile * Q (blocked WY), then
