@@ -175,28 +175,40 @@ class CompressPlan:
         out[0] = self.status[off:off + 1]
         return out
 
-    def run(self, omega, psi, y, z, stream=None):
-        """Enqueue the level sweep (compress.py:250-279) on `stream`."""
+    def run_level(self, idx, quad, stream, box_range=None, chunk_geo=None, status=None):
+        """Enqueue one level (spec index `idx`) on `stream`; `box_range` =
+        (b0, b1) restricts it to a contiguous run of boxes (whose geometry
+        `chunk_geo` holds rows relative to box b0).  Returns the lift buffers."""
         lib = _native.lib()
-        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        level = self.specs[idx][0]
         r, s = self.rank, self.s
-        stat = self._status_slices()
+        g = self.geometry[level]
+        u, v, d = self.levels[level]
+        out = self.lift[idx % 2]
+        if box_range is None:
+            b0, geo, row0, sq0, stat = 0, g, 0, 0, self._status_slices()[level]
+        else:
+            b0, b1 = box_range
+            geo, row0, sq0 = chunk_geo, int(g.begins_host[b0] - g.begins_host[0]), int(g.sq_host[b0])
+            stat = status
+        q = [m[row0:] for m in quad]
+        rc = lib.hbs_compress_level(
+            geo.nbox, geo.row_begin.data_ptr(), geo.sq_off.data_ptr(), geo.max_rows, s, r, self.tol,
+            q[0].data_ptr(), q[1].data_ptr(), q[2].data_ptr(), q[3].data_ptr(),
+            u[row0:].data_ptr(), v[row0:].data_ptr(), d[sq0:].data_ptr(),
+            out[0][b0 * r:].data_ptr(), out[1][b0 * r:].data_ptr(), out[2][b0 * r:].data_ptr(),
+            out[3][b0 * r:].data_ptr(),
+            self.workspace.data_ptr(), self.workspace_bytes, stat.data_ptr(), stream)
+        _native.check(rc, f"hbs_compress_level(level {level})")
+        return tuple(m[:g.nbox * r] for m in out)
+
+    def run(self, omega, psi, y, z, stream=None, first=0):
+        """Enqueue the level sweep (compress.py:250-279) on `stream`, from spec
+        index `first` (the quadruple given is that level's input)."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         quad = (omega, psi, y, z)
-        for idx, (level, _, _) in enumerate(self.specs):
-            g = self.geometry[level]
-            u, v, d = self.levels[level]
-            out = self.lift[idx % 2]
-            rc = lib.hbs_compress_level(
-                g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.max_rows, s, r, self.tol,
-                quad[0].data_ptr(), quad[1].data_ptr(), quad[2].data_ptr(), quad[3].data_ptr(),
-                u.data_ptr(), v.data_ptr(), d.data_ptr(),
-                out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), out[3].data_ptr(),
-                self.workspace.data_ptr(), self.workspace_bytes, stat[level].data_ptr(), st)
-            _native.check(rc, f"hbs_compress_level(level {level})")
-            rows = g.nbox * r
-            quad = tuple(m[:rows] for m in out)
-        if not self.specs:
-            quad = (omega, psi, y, z)
+        for idx in range(first, len(self.specs)):
+            quad = self.run_level(idx, quad, st)
         self.top_quad = quad
         if self.with_root:
             self.run_root(quad[0], quad[2], stream=st)
@@ -229,6 +241,23 @@ class CompressPlan:
         if self.with_root and host[off]:
             return 0, 0
         return None
+
+    def raise_for_status_from(self, first_idx):
+        """Like raise_for_status but ignoring the specs before `first_idx`
+        (their statuses were checked elsewhere, e.g. per leaf chunk)."""
+        host = self.status.cpu().numpy()
+        off = 0
+        for idx, (level, _, _) in enumerate(self.specs):
+            nbox = self.geometry[level].nbox
+            blk = host[off:off + 2 * nbox].reshape(2, nbox)
+            off += 2 * nbox
+            if idx < first_idx:
+                continue
+            bad = np.nonzero(blk.any(axis=0))[0]
+            if bad.size:
+                raise_ill_conditioned(level, (1 << level) - 1 + self.first_box[level] + int(bad[0]), self.tol)
+        if self.with_root and host[off]:
+            raise_ill_conditioned(0, 0, self.tol)
 
     def raise_for_status(self):
         """Raise like the reference for the first failing node in sweep order."""
@@ -291,6 +320,96 @@ def _charge_madds(tree: ClusterTree, s: int, r: int):
     flops.add_madds(total)
 
 
+def _pinned_view(a):
+    """torch view of a numpy array if it lives in pinned host memory, else None."""
+    if isinstance(a, torch.Tensor):
+        return None
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    return t if t.is_pinned() else None
+
+
+def _compress_host_pipelined(host, tree: ClusterTree, config: CompressionConfig, dev, chunks: int = 8):
+    """Host (pinned) samples in, host-materialised factorization out, with the
+    transfers overlapped: the leaf level streams in `chunks` runs of boxes
+    (H2D of run c+1 on a copy stream while run c computes), and every level's
+    U, V, D go back to pinned host memory on the copy stream as soon as they
+    are final, while the coarser levels compute."""
+    from .factorization import LevelGeometry
+    n, s = host[0].shape
+    r, tol = config.rank, config.ill_conditioning_tol
+    plan = CompressPlan(tree, s, r, tol, dev)
+    comp = torch.cuda.current_stream(dev)
+    h2d = torch.cuda.Stream(dev)      # separate copy streams: PCIe is full duplex
+    copy = torch.cuda.Stream(dev)     # device -> host
+    L = tree.depth
+    g = plan.geometry[L]
+    nb = g.nbox
+    chunks = max(1, min(chunks, nb))
+    edges = [round(i * nb / chunks) for i in range(chunks + 1)]
+    dq = [torch.empty(n, s, dtype=torch.float64, device=dev) for _ in range(4)]
+    # per-level pinned destinations
+    hosts = {}
+    for lv, (u, v, d) in plan.levels.items():
+        hosts[lv] = tuple(torch.empty(t.shape, dtype=torch.float64, pin_memory=True) for t in (u, v, d))
+    statuses, evs, arrived = [], [], []
+    for c in range(chunks):       # all uploads first, back to back on the H2D stream
+        b0, b1 = edges[c], edges[c + 1]
+        r0, r1 = int(g.begins_host[b0]), int(g.begins_host[b1])
+        with torch.cuda.stream(h2d):
+            for i in range(4):
+                dq[i][r0:r1].copy_(host[i][r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        arrived.append(ev)
+    geos = [LevelGeometry(g.begins_host[edges[c]:edges[c + 1] + 1], dev) for c in range(chunks)]
+    for c in range(chunks):
+        b0, b1 = edges[c], edges[c + 1]
+        r0, r1 = int(g.begins_host[b0]), int(g.begins_host[b1])
+        ev, geo = arrived[c], geos[c]
+        stat = torch.zeros(2 * (b1 - b0), dtype=torch.int32, device=dev)
+        comp.wait_event(ev)
+        plan.run_level(0, dq, comp.cuda_stream, box_range=(b0, b1), chunk_geo=geo, status=stat)
+        done = torch.cuda.Event()
+        done.record(comp)
+        copy.wait_event(done)
+        u, v, d = plan.levels[L]
+        hu, hv, hd = hosts[L]
+        sq0, sq1 = int(g.sq_host[b0]), int(g.sq_host[b1])
+        with torch.cuda.stream(copy):
+            hu[r0:r1].copy_(u[r0:r1], non_blocking=True)
+            hv[r0:r1].copy_(v[r0:r1], non_blocking=True)
+            hd[sq0:sq1].copy_(d[sq0:sq1], non_blocking=True)
+        statuses.append((b0, stat))
+        evs.append((geo, ev, done))
+    quad = tuple(m[:nb * r] for m in plan.lift[0])
+    for idx in range(1, len(plan.specs)):
+        quad = plan.run_level(idx, quad, comp.cuda_stream)
+        lv = plan.specs[idx][0]
+        done = torch.cuda.Event()
+        done.record(comp)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            for t, h in zip(plan.levels[lv], hosts[lv]):
+                h.copy_(t, non_blocking=True)
+    plan.top_quad = quad
+    plan.run_root(quad[0], quad[2], stream=comp.cuda_stream)
+    torch.cuda.synchronize(dev)
+    # failures in sweep order: leaf chunks first (ascending boxes), then the rest
+    for b0, stat in statuses:
+        hs = stat.cpu().numpy()
+        k = hs.size // 2
+        bad = np.nonzero(hs.reshape(2, k).any(axis=0))[0]
+        if bad.size:
+            raise_ill_conditioned(L, (1 << L) - 1 + b0 + int(bad[0]), tol)
+    plan.raise_for_status_from(1)
+    f = plan.factorization()
+    for lv, (hu, hv, hd) in hosts.items():
+        f._host[(lv, "u")], f._host[(lv, "v")], f._host[(lv, "d")] = hu.numpy(), hv.numpy(), hd.numpy()
+    f._host["root"] = plan.root.cpu().numpy()
+    f._host_keepalive = (hosts, dq)
+    return f
+
+
 def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: CompressionConfig,
                           device=None) -> HbsFactorization:
     """Level sweep on an already-drawn probe quadruple (compress.py:236-280),
@@ -306,6 +425,12 @@ def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: Compres
         dev = torch.device(device)
     if dev.type != "cuda":
         raise DimensionError("the compressor runs on a CUDA device only (no CPU fallback)")
+    pinned = [_pinned_view(m) for m in (samples.omega, samples.psi, samples.y, samples.z)]
+    if all(p is not None for p in pinned) and tree.depth >= 2:
+        f = _compress_host_pipelined(pinned, tree, config, dev)
+        if flops.counting():
+            _charge_madds(tree, s, r)
+        return f
     quad = [_device_tensor(m, dev) for m in (samples.omega, samples.psi, samples.y, samples.z)]
     plan = CompressPlan(tree, s, r, config.ill_conditioning_tol, dev)
     plan.run(*quad)

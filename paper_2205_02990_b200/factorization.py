@@ -154,10 +154,14 @@ class HbsFactorization:
         pending, nbytes = [], 0
         for level in range(1, self.tree.depth + 1):
             for kind, t in zip("uvd", self.levels[level]):
+                nbytes_t = t.numel() * 8
+                if (level, kind) in self._host:      # already on the host (pipelined compress)
+                    nbytes += nbytes_t
+                    continue
                 h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                 h.copy_(t, non_blocking=True)
                 pending.append(((level, kind), h))
-                nbytes += t.numel() * 8
+                nbytes += nbytes_t
         root = torch.empty(self.root_device.shape, dtype=torch.float64, pin_memory=True)
         root.copy_(self.root_device, non_blocking=True)
         nbytes += root.numel() * 8

@@ -221,3 +221,40 @@ def test_hbsf_round_trip_device(tmp_path):
     g = load_factorization(tmp_path / "f.hbsf")
     x = c["x"]
     assert np.array_equal(hb.apply_matrix(f, x), hb.apply_matrix(g, x))
+
+
+def _pinned(a):
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    t.copy_(torch.from_numpy(a))
+    return t
+
+
+@pytest.mark.parametrize("name", ["c1_twin", "uneven_333", "c4_shape_literal"])
+def test_pinned_host_pipeline_bitwise(name):
+    """Pinned host samples take the overlapped path (chunked leaf uploads,
+    per-level downloads on a second stream); results equal the plain path
+    bit for bit, and the dict views come back already on the host."""
+    c = golden_cases.load(name)
+    tree = hb.build_tree(c["n"], c["leaf"])
+    cfg = hb.CompressionConfig(rank=c["r"], leaf_threshold=c["leaf"])
+    plain = hb.compress_from_samples(hb.SampleSet(*c["samples"]), tree, cfg)
+    keep = [_pinned(m) for m in c["samples"]]
+    piped = hb.compress_from_samples(hb.SampleSet(*(t.numpy() for t in keep)), tree, cfg)
+    assert ("root" in piped._host) and all((lv, "d") in piped._host for lv in range(1, tree.depth + 1))
+    assert np.array_equal(plain.root_disc, piped.root_disc)
+    for nid in plain.u_bases:
+        assert np.array_equal(plain.u_bases[nid], piped.u_bases[nid])
+        assert np.array_equal(plain.discs[nid], piped.discs[nid])
+
+
+def test_pinned_host_pipeline_failure_names_node():
+    n, m = 4096, 32
+    g = O.baseline_generator(n, m, 16, seed=0)
+    om, ps, y, z = O.samples_from(g, 72, 0)
+    lo = int(O.level_bounds(n, 7)[7][77])
+    om[lo + 1] = om[lo]
+    keep = [_pinned(a) for a in (om, ps, y, z)]
+    with pytest.raises(hb.IllConditionedProbeError) as exc:
+        hb.compress_from_samples(hb.SampleSet(*(t.numpy() for t in keep)), hb.build_tree(n, m),
+                                 hb.CompressionConfig(rank=24, leaf_threshold=m))
+    assert exc.value.level == 7 and exc.value.node_id == 127 + 77
