@@ -96,6 +96,18 @@ HBS_DEV void mbar_wait_warp(uint64_t* bar, unsigned parity) {
   __syncwarp();
 }
 
+// TMA bulk copy global -> shared with mbarrier completion (cp.async.bulk).
+HBS_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+HBS_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+
 // cp.async (LDGSTS) helpers: 8-byte element copies with zero fill.
 HBS_DEV void cp_async8(double* dst, const double* src, bool pred) {
   const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));

@@ -540,28 +540,177 @@ HBS_DEV void panel_factor_wide(double* A, int lda, int m, int j0, int nbp, doubl
 }
 
 // Panel factorisation with 8-lane column groups (warps 0..7 of the CTA).
-// Lane group lg = lane / 8 of warp w owns panel column q = w + 8 lg; lane
+// Lane group lg = lane / 8 of warp w owns panel column q = 4w + lg; lane
 // li = lane % 8 of the group holds rows j0 + li + 8k (k < MR8) in registers.
 // Every column-dot reduction is a 3-stage xor shuffle inside the group, and
-// the four groups of a warp reduce in the same shuffle instructions, so a
-// step costs each warp 6 shuffles instead of 10 per column (the SM's shuffle
-// throughput, not latency, limited the 32-lane layout).  Step j needs only
-// pivot j (mbarrier hand-off, as in panel_factor_wide); retired columns form
-// the compact-WY dots G(q, j) in the same reductions.
+// the four groups of a warp reduce in the same shuffle instructions.  Step j
+// needs only pivot j (mbarrier hand-off from the warp owning it); a step is
+// bound by the FP64 and shuffle/shared pipes the active warps share, so warp
+// w stops after step 4w+3 (its columns are all reflectors by then) and only
+// the publishing warp runs the next pivot's norm.  The compact-WY dots
+// V^T V for form_t come from one tensor-core Gram product afterwards.
+template <int NTG>
+HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G);
+
+// Transposed butterfly: four per-lane partial sums -> on return lanes
+// 8s .. 8s+7 hold the warp-wide sum of slot s = lane >> 3 (6 shuffles, 5 stages).
+HBS_DEV double reduce4_t(const double (&a)[4], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8;
+  const double k0 = (b4 ? a[2] : a[0]) + __shfl_xor_sync(0xffffffffu, b4 ? a[0] : a[2], 16);
+  const double k1 = (b4 ? a[3] : a[1]) + __shfl_xor_sync(0xffffffffu, b4 ? a[1] : a[3], 16);
+  double k = (b3 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;
+}
+
+// Panel factorisation with warp-local column blocks (warps 0..7 of the group).
+// Warp w holds panel columns 4w .. 4w+3 in registers, lane l rows j0 + l + 32k.
+// It first applies the reflectors of the earlier warps' columns as they are
+// published (mbarrier per reflector, one step behind the producer), then
+// factors its own four columns with no cross-warp traffic: a step is the
+// pivot's dots, one transposed 4-slot butterfly, the rank-1 update and the
+// next pivot's norm by the update formula (exact recomputation on
+// cancellation), so only every fourth pivot crosses warps.  Published
+// columns hold the final R entries, beta and the dlarfg-scaled tails; the
+// compact-WY dots V^T V for form_t come from one tensor-core Gram product.
+template <int MR, int NTG>
+HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                            double* s_beta, uint64_t* bar, unsigned parity, double* G) {
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31;
+  if (warp < ((nbp + 3) >> 2)) {
+    const int cb = 4 * warp;     // my first panel column
+    const int mr = m - j0;       // panel rows; relative row of (lane, k) = lane + 32 k
+    double x[4][MR];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        x[c][k] = (cb + c < nbp && row < mr) ? A[(j0 + row) + (j0 + cb + c) * lda] : 0.0;
+      }
+    // reflectors 0 .. cb-1 (earlier warps), applied as they are published
+    for (int j = 0; j < cb; ++j) {
+      mbar_wait(&bar[j], parity);
+      const double tau = s_tau[j0 + j];
+      double v[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        v[k] = (row > j && row < mr) ? A[(j0 + row) + (j0 + j) * lda] : (row == j ? 1.0 : 0.0);
+      }
+      double pc[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          if (k & 1) a1 = fma(v[k], x[c][k], a1);
+          else a0 = fma(v[k], x[c][k], a0);
+        }
+        pc[c] = a0 + a1;
+      }
+      const double tot = tau * reduce4_t(pc, lane);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double w = __shfl_sync(0xffffffffu, tot, 8 * c);
+#pragma unroll
+        for (int k = 0; k < MR; ++k) x[c][k] = fma(-w, v[k], x[c][k]);
+      }
+    }
+    // my first pivot: exact norm below row cb, alpha = row cb (lane cb, slot 0)
+    double nrm, alpha;
+    {
+      double pp = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (lane + 32 * k > cb) pp = fma(x[0][k], x[0][k], pp);
+      nrm = warp_sum(pp);
+      alpha = __shfl_sync(0xffffffffu, x[0][0], cb);
+    }
+#pragma unroll
+    for (int jl = 0; jl < 4; ++jl) {
+      const int j = cb + jl;
+      if (j >= nbp) break;
+      const Reflector h = make_reflector(alpha, nrm);
+      double pv[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) pv[k] = (lane + 32 * k > j) ? x[jl][k] : 0.0;
+      double pc[4] = {0.0, 0.0, 0.0, 0.0}, r[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = jl + 1; c < 4; ++c) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          if (k & 1) a1 = fma(pv[k], x[c][k], a1);
+          else a0 = fma(pv[k], x[c][k], a0);
+        }
+        pc[c] = a0 + a1;
+        r[c] = __shfl_sync(0xffffffffu, x[c][0], j);   // row j of column c
+      }
+      // next pivot (column jl+1): ||x||^2, ||pv||^2 over rows > j+1, row j+1 values
+      double sxx = 0.0, spp = 0.0, xn_old = 0.0, pn = 0.0;
+      if (jl < 3) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (lane + 32 * k > j + 1) { sxx = fma(x[jl + 1][k], x[jl + 1][k], sxx); spp = fma(pv[k], pv[k], spp); }
+        xn_old = __shfl_sync(0xffffffffu, x[jl + 1][0], j + 1);
+        pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+      }
+      const double dsum = reduce4_t(pc, lane);
+      if (jl < 3) { sxx = warp_sum(sxx); spp = warp_sum(spp); }
+      double gsn = 0.0, dn = 0.0;
+#pragma unroll
+      for (int c = jl + 1; c < 4; ++c) {
+        const double dc = __shfl_sync(0xffffffffu, dsum, 8 * c);
+        const double f = h.tau * (r[c] + h.scale * dc), gs = f * h.scale;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) x[c][k] = fma(-gs, pv[k], x[c][k]);
+        if (lane == j) x[c][0] -= f;
+        if (c == jl + 1) { gsn = gs; dn = dc; }
+      }
+      if (jl < 3 && j + 1 < nbp) {
+        // ||x'||^2 = sxx - 2 gs (x . pv) + gs^2 spp over rows > j+1
+        double nn = fma(gsn * gsn, spp, fma(-2.0 * gsn, dn - pn * xn_old, sxx));
+        alpha = fma(-gsn, pn, xn_old);
+        if (!(nn > 0.5 * sxx) || sxx == 0.0) {   // warp-uniform
+          double pp = 0.0;
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (lane + 32 * k > j + 1) pp = fma(x[jl + 1][k], x[jl + 1][k], pp);
+          nn = warp_sum(pp);
+        }
+        nrm = nn;
+      }
+      // publish column j: R above, beta on the diagonal, scaled tail below
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        if (row < mr) A[(j0 + row) + (j0 + j) * lda] = row < j ? x[jl][k] : (row == j ? h.beta : x[jl][k] * h.scale);
+      }
+      if (lane == 0) { s_tau[j0 + j] = h.tau; s_scale[j0 + j] = h.scale; s_beta[j0 + j] = h.beta; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[j]);
+    }
+  }
+  gsync<NTG>();
+  panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
+  gsync<NTG>();
+}
+
 template <int MR8, int NTG>
 HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
                             double* s_beta, uint64_t* bar, unsigned parity, double* G, double* s_an) {
   // s_an[j] = alpha (pre-reflection diagonal), s_an[32 + j] = ||x||^2 of pivot j:
   // the publisher stores only these; every warp forms the reflector itself,
   // overlapped with its own loads and reductions (off the critical chain).
-  // G(q, j) is only written for q < j < nbp; zero it so form_t never reads
-  // stale shared memory for partial panels.
-  for (int e = ltid<NTG>(); e < kP * kLdT; e += gthreads<NTG>()) G[e] = 0.0;
-  gsync<NTG>();
   const int warp = (ltid<NTG>() >> 5), lane = ltid<NTG>() & 31;
   if (warp < 8) {
     const int lg = lane >> 3, li = lane & 7, gbase = lane & 24;
-    const int q = warp + 8 * lg, c = j0 + q;
+    // contiguous columns per warp: warp w retires after step 4w+3 and leaves
+    // the pipes to the warps still updating
+    const int q = 4 * warp + lg, c = j0 + q, jlast = 4 * warp + 3;
     const bool own = q < nbp;
     const int kc = (m - j0 + 7) >> 3;
     double x[MR8];
@@ -585,88 +734,93 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
     for (int kb = 0; kb < 4; ++kb) {          // row slot of the pivot: kb = j / 8 (compile time)
       for (int jl = 0; jl < 8; ++jl) {
         const int j = 8 * kb + jl, jj = j0 + j;
-        if (j >= nbp) break;
+        if (j >= nbp || j > jlast) break;
         const bool tr = (j == 6) && own && (q == 7) && li == 0;
-        if (tr) STEP_MARK(0);
+        // warp-uniform: this warp owns pivot j+1 (group (j+1)%4 of warp (j+1)/4).
+        // Only it runs the norm / publish work and its shuffles: the SM's
+        // shuffle and shared-memory pipes, shared by the eight warps, bound a step.
+        const bool pubw = warp == ((j + 1) >> 2) && j + 1 < nbp;
         mbar_wait(&bar[j], parity);
-        if (tr) STEP_MARK(1);
-        const Reflector hj = make_reflector(s_an[j], s_an[32 + j]);
-        const double tau = hj.tau, scale = hj.scale;
-        if (c == jj && li == 0) { s_tau[jj] = hj.tau; s_scale[jj] = hj.scale; s_beta[jj] = hj.beta; }
+        if (tr) STEP_MARK(0);
         double pv[MR8];
 #pragma unroll
         for (int k = 0; k < MR8; ++k) {
           const int row = j0 + li + 8 * k;
           pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
         }
+        const Reflector hj = make_reflector(s_an[j], s_an[32 + j]);
+        const double tau = hj.tau, scale = hj.scale;
+        if (tr) STEP_MARK(1);
+        if (c == jj && li == 0) { s_tau[jj] = hj.tau; s_scale[jj] = hj.scale; s_beta[jj] = hj.beta; }
+        if (tr) STEP_MARK(2);
         const bool pub = own && (q == j + 1);
-        // my value in row jj (slot kb, lane jl of my group) and in row jj+1
+        // my value in row jj (slot kb, lane jl of my group)
         const double r = __shfl_sync(0xffffffffu, x[kb], gbase | jl);
-        const double xn_old = (jl == 7) ? __shfl_sync(0xffffffffu, x[kb < 3 ? kb + 1 : kb], gbase)
-                                        : __shfl_sync(0xffffffffu, x[kb], gbase | (jl + 1));
-        const double pn = (jl == 7) ? __shfl_sync(0xffffffffu, pv[kb < 3 ? kb + 1 : kb], gbase)
-                                    : __shfl_sync(0xffffffffu, pv[kb], gbase | (jl + 1));
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, sxx = 0.0, spp = 0.0;
+        double dd[8] = {};
 #pragma unroll
-        for (int k = 0; k < MR8; k += 4) {
-          d0 = fma(pv[k], x[k], d0);
-          if (k + 1 < MR8) d1 = fma(pv[k + 1], x[k + 1], d1);
-          if (k + 2 < MR8) d2 = fma(pv[k + 2], x[k + 2], d2);
-          if (k + 3 < MR8) d3 = fma(pv[k + 3], x[k + 3], d3);
-        }
-        if (pub) {
+        for (int k = 0; k < MR8; ++k) dd[k & 7] = fma(pv[k], x[k], dd[k & 7]);
+        if (tr) STEP_MARK(3);
+        double d = ((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]));
+        // publisher warp: ||x||^2 and ||pv||^2 over rows > jj+1 (pre-update x),
+        // and the row-(jj+1) values of x and pv
+        double sxx = 0.0, spp = 0.0, xn_old = 0.0, pn = 0.0;
+        if (pubw) {
+          double sx[4] = {}, sp[4] = {};
 #pragma unroll
           for (int k = 0; k < MR8; ++k)
-            if (li + 8 * k > j + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
+            if (li + 8 * k > j + 1) { sx[k & 3] = fma(x[k], x[k], sx[k & 3]); sp[k & 3] = fma(pv[k], pv[k], sp[k & 3]); }
+          sxx = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+          spp = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+          const int nl = (jl == 7) ? gbase : (gbase | (jl + 1));
+          xn_old = __shfl_sync(0xffffffffu, (jl == 7) ? x[kb < 3 ? kb + 1 : kb] : x[kb], nl);
+          pn = __shfl_sync(0xffffffffu, (jl == 7) ? pv[kb < 3 ? kb + 1 : kb] : pv[kb], nl);
         }
-        if (tr) STEP_MARK(2);
-        double d = (d0 + d1) + (d2 + d3);
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          d += __shfl_xor_sync(0xffffffffu, d, o);
-          sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
-          spp += __shfl_xor_sync(0xffffffffu, spp, o);
-        }
-        if (tr) STEP_MARK(3);
-        // Branch-light step: every shuffle / warp sync below is executed by the
-        // whole warp (partial-mask shuffles in divergent code compile to the
-        // slow WARPSYNC.COLLECTIVE emulation).
+        d += __shfl_xor_sync(0xffffffffu, d, 4);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        if (tr) STEP_MARK(4);
         const double f = tau * (r + scale * d), gs = f * scale;
-        if (own && c < jj && li == 0) G[q * kLdT + j] = s_scale[c] * (r + scale * d);   // compact-WY dot
         if (own && c > jj) {
 #pragma unroll
           for (int k = 0; k < MR8; ++k) x[k] = fma(-gs, pv[k], x[k]);
           if (li == jl) x[kb] -= f;
         }
-        if (tr) STEP_MARK(4);
-        // next pivot: ||x'||^2 over rows > jj+1 = sxx - 2 gs sxp + gs^2 spp, exact on cancellation
-        double nrm = fma(gs * gs, spp, fma(-2.0 * gs, d - pn * xn_old, sxx));
-        const bool need = pub && (!(nrm > 0.5 * sxx) || sxx == 0.0);
-        if (__any_sync(0xffffffffu, need)) {
-          double pp = 0.0;
-#pragma unroll
-          for (int k = 0; k < MR8; ++k)
-            if (k < kc && li + 8 * k > j + 1) pp = fma(x[k], x[k], pp);
-          pp += __shfl_xor_sync(0xffffffffu, pp, 4);
-          pp += __shfl_xor_sync(0xffffffffu, pp, 2);
-          pp += __shfl_xor_sync(0xffffffffu, pp, 1);
-          if (need) nrm = pp;
-        }
-        const double alpha = (jl == 7) ? __shfl_sync(0xffffffffu, x[kb < 3 ? kb + 1 : kb], gbase)
-                                       : __shfl_sync(0xffffffffu, x[kb], gbase | (jl + 1));
-        if (pub) {
-#pragma unroll
-          for (int k = 0; k < MR8; ++k)
-            if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
-        }
         if (tr) STEP_MARK(5);
-        if (__any_sync(0xffffffffu, pub)) {
+        if (pubw) {
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 4);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 4);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 2);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 2);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 1);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 1);
+          // next pivot: ||x'||^2 over rows > jj+1 = sxx - 2 gs sxp + gs^2 spp,
+          // recomputed exactly on cancellation; alpha = updated row jj+1
+          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, d - pn * xn_old, sxx));
+          const double alpha = fma(-gs, pn, xn_old);
+          if (tr) STEP_MARK(6);
+          const bool need = pub && (!(nrm > 0.5 * sxx) || sxx == 0.0);
+          if (__any_sync(0xffffffffu, need)) {
+            double pp = 0.0;
+#pragma unroll
+            for (int k = 0; k < MR8; ++k)
+              if (k < kc && li + 8 * k > j + 1) pp = fma(x[k], x[k], pp);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 4);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 2);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 1);
+            if (need) nrm = pp;
+          }
+          if (tr) STEP_MARK(7);
+          if (pub) {
+#pragma unroll
+            for (int k = 0; k < MR8; ++k)
+              if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
+          }
           __syncwarp();
           if (pub && li == 0) {
             s_an[j + 1] = alpha; s_an[32 + j + 1] = nrm;
-            if (tr) STEP_MARK(6);
+            if (tr) STEP_MARK(8);
             mbar_arrive(&bar[j + 1]);
-            if (tr) STEP_MARK(7);
+            if (tr) STEP_MARK(9);
           }
         }
       }
@@ -686,6 +840,8 @@ HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* 
       else A[i + cc * lda] = s_beta[cc];
     }
   }
+  gsync<NTG>();
+  panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
   gsync<NTG>();
 }
 
@@ -857,7 +1013,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hqr_kernel(GeqrfArgs args) {
     const int j0 = p * kP, nbp = min(kP, n - j0);
     double* T = Tbase + (args.mode == kGeqrfOrtho ? p * kP * kLdT : 0);
     HQR_MARK(2 + 4 * p);
-    if constexpr (MR <= 6) panel_factor_q<MR * 4, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G, Tscr + 320);
+    if constexpr (MR <= 6) panel_factor_r<MR, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
     else panel_factor_wide<MR, NT / 32, 0>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
     HQR_MARK(3 + 4 * p);
     form_t<0>(T, Tscr, G, s_tau, j0, nbp);
@@ -1138,29 +1294,102 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   double* s_beta = s_scale + args.n_max;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + args.n_max);   // 32 step barriers
   uint64_t* s_ready = s_bar + kP;                                          // 16 panel-ready + 1 R-ready
-  double* G = smem + round_up(3 * args.n_max + kP + 32, 2);
+  double* G = smem + round_up(3 * args.n_max + kP + 34, 2);
   double* Tscr = G + kP * kLdT;
   double* T = Tscr + 384;
   double* A = T + round_up(kP * kLdT, 2);
 
-  // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1
+  // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1.
+  // Each column is one contiguous Omega row: TMA bulk copies (one per column)
+  // completing on an mbarrier when rows are 16-byte aligned, else cp.async.
   const double* src = S.om + S.om_c_rb * rb;
-  for (int j = 0; j < n; ++j)
-    for (int i = threadIdx.x; i < mpad; i += blockDim.x) {
-      const bool ok = i < m;
-      cp_async8(&A[i + j * lda], ok ? src + (int64_t)j * s + i : src, ok);
-    }
-  cp_async_commit();
-  if (threadIdx.x < kP + 32) mbar_init(&s_bar[threadIdx.x], 1);
+  uint64_t* s_load = s_ready + 33;
+  const bool bulk = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((lda & 1) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  if (threadIdx.x < kP + 34) mbar_init(&s_bar[threadIdx.x], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  cp_async_wait<0>();
+  __syncthreads();
+  if (bulk) {
+    if (threadIdx.x == 0) mbar_expect_tx(s_load, (unsigned)(n * m * sizeof(double)));
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      bulk_g2s(&A[j * lda], src + (int64_t)j * s, (unsigned)(m * sizeof(double)), s_load);
+    const int zr = mpad - m;
+    for (int e = threadIdx.x; e < zr * n; e += blockDim.x) A[m + e % zr + (e / zr) * lda] = 0.0;
+    mbar_wait(s_load, 0);
+  } else {
+    for (int j = 0; j < n; ++j)
+      for (int i = threadIdx.x; i < mpad; i += blockDim.x) {
+        const bool ok = i < m;
+        cp_async8(&A[i + j * lda], ok ? src + (int64_t)j * s + i : src, ok);
+      }
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
   __syncthreads();
 
   double* tglob = S.t + (size_t)b * S.t_stride;
   double* rglob = S.rinv + (size_t)b * S.rinv_stride;
   if (threadIdx.x == 0) FUSED_MARK(0);
+  double* yq = S.yq + (size_t)b * S.yq_stride;
+  const int ngroups = (nb + 7) >> 3;
+  // blocked back substitution X R^T = Y Q1 for one 8-row group, in place in
+  // YQ (columns < n); R from shared memory, inverse diagonal blocks from rglob
+  auto solve_rows = [&](int rg) {
+    const int row = 8 * rg + g;
+    const bool rok = row < nb;
+    double* drow = yq + (size_t)row * s;
+    for (int blk = npanel - 1; blk >= 0; --blk) {
+      const int i0 = blk * kP, c0 = i0 + kP;
+      const int kr = n > c0 ? round_up(n - c0, 4) : 0;
+      double acc[4][2];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = i0 + 8 * f + 2 * t + e;
+          acc[f][e] = (rok && c < n) ? __ldcg(drow + c) : 0.0;
+        }
+      for (int kc = 0; kc < kr; kc += 32) {
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + kc + 4 * u + t;
+          av[u] = (rok && c < n) ? -__ldcg(drow + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (kc + 4 * u >= kr) break;
+          const int c = c0 + kc + 4 * u + t;
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const int i = i0 + 8 * f + g;
+            const double bv = (i < n && c < n) ? A[i + c * lda] : 0.0;   // R(i, c), upper part
+            dmma8x8x4(acc[f][0], acc[f][1], av[u], bv);
+          }
+        }
+      }
+      const double* ri = rglob + (size_t)blk * kP * kP;
+      double xb[4][2] = {};
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        const double a = cfrag_to_afrag<4>(acc, kk, lane);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) dmma8x8x4(xb[f][0], xb[f][1], a, __ldcg(ri + (8 * f + g) * kP + kk + t));
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = i0 + 8 * f + 2 * t + e;
+          if (rok && c < n) drow[c] = xb[f][e];
+        }
+      __syncwarp();
+    }
+  };
   // s_ready[p] (p < 16): panel p factored (P -> Y);  s_ready[16 + p]: far
-  // trailing update of panel p done (Y -> P); p < 8 for the latter.
+  // trailing update of panel p done (Y -> P);  s_ready[32]: all panels
+  // applied to YQ (Y -> P);  s_ready[33]: operand load (TMA).
   if (warp >= 8) {
     // ------------------------------------------------------------ group P
     // (physical warps 8..15 = logical 0..7: the arbiter favours high warp ids)
@@ -1176,7 +1405,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         gsync<256>();
       }
       if (lt == 0) FUSED_MARK(22 + 2 * p);
-      if constexpr (MR <= 6) panel_factor_q<MR * 4, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G, Tscr + 320);
+      if constexpr (MR <= 6) panel_factor_r<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
       else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
       if (lt == 0) FUSED_MARK(42 + p);
       form_t<256>(T, Tscr, G, s_tau, j0, nbp);
@@ -1200,6 +1429,10 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         FUSED_MARK(20);
       }
     }
+    // group Y has applied every panel and inverted every diagonal block of R:
+    // take row groups lt/32 (mod 16) of the solve
+    mbar_wait(&s_ready[32], 0);
+    for (int rg = lt >> 5; rg < ngroups; rg += 16) solve_rows(rg);
     return;
   }
 
@@ -1211,10 +1444,11 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     mbar_wait(&s_ready[p], 0);
     if (p * kP + 2 * kP < n) { ysync<256, 2>(); if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]); }
   }
+  ysync<256, 2>();
+  if (yw == 0 && lane == 0) mbar_arrive(&s_ready[32]);
   return;
 #endif
   const double* y0 = S.y + S.y_c_rb * rb;
-  double* yq = S.yq + (size_t)b * S.yq_stride;
   // 16-byte vector accesses only when every row start is 16-byte aligned
   const bool vec2 = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(y0) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(yq) & 15) == 0);
@@ -1229,7 +1463,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     else { p[0] = v.x; if (second) p[1] = v.y; }
   };
   const int spad = round_up(s, 8);
-  const int ngroups = (nb + 7) >> 3;
   for (int p = 0; p < npanel; ++p) {
     const int j0 = p * kP, nbp = min(kP, n - j0), kb = j0 & ~7;
     mbar_wait(&s_ready[p], 0);
@@ -1327,74 +1560,25 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     }
     if (yw == 0 && lane == 0) FUSED_MARK(30 + p);
   }
-  // blocked back substitution X R^T = Y Q1, in place in YQ (columns < n)
+  // blocked back substitution, row groups shared with group P (which is idle
+  // once its last panel is factored): Y takes rg = 8 + yw (mod 16)
+  __threadfence_block();
   ysync<256, 2>();
-  if (yw == 0 && lane == 0) FUSED_MARK(40);
-  for (int rg = yw; rg < ngroups; rg += 8) {
-    const int row = 8 * rg + g;
-    const bool rok = row < nb;
-    double* drow = yq + (size_t)row * s;
-    for (int blk = npanel - 1; blk >= 0; --blk) {
-      const int i0 = blk * kP, c0 = i0 + kP;
-      const int kr = n > c0 ? round_up(n - c0, 4) : 0;
-      double acc[4][2];
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = i0 + 8 * f + 2 * t + e;
-          acc[f][e] = (rok && c < n) ? __ldcg(drow + c) : 0.0;
-        }
-      for (int kc = 0; kc < kr; kc += 32) {
-        double av[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = c0 + kc + 4 * u + t;
-          av[u] = (rok && c < n) ? -__ldcg(drow + c) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (kc + 4 * u >= kr) break;
-          const int c = c0 + kc + 4 * u + t;
-#pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            const int i = i0 + 8 * f + g;
-            const double bv = (i < n && c < n) ? A[i + c * lda] : 0.0;   // R(i, c), upper part
-            dmma8x8x4(acc[f][0], acc[f][1], av[u], bv);
-          }
-        }
-      }
-      const double* ri = rglob + (size_t)blk * kP * kP;
-      double xb[4][2] = {};
-#pragma unroll
-      for (int kk = 0; kk < kP; kk += 4) {
-        const double a = cfrag_to_afrag<4>(acc, kk, lane);
-#pragma unroll
-        for (int f = 0; f < 4; ++f) dmma8x8x4(xb[f][0], xb[f][1], a, __ldcg(ri + (8 * f + g) * kP + kk + t));
-      }
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = i0 + 8 * f + 2 * t + e;
-          if (rok && c < n) drow[c] = xb[f][e];
-        }
-      __syncwarp();
-    }
-  }
+  if (yw == 0 && lane == 0) { mbar_arrive(&s_ready[32]); FUSED_MARK(40); }
+  for (int rg = 8 + yw; rg < ngroups; rg += 16) solve_rows(rg);
   if (yw == 0 && lane == 0) FUSED_MARK(41);
 }
 
 bool fused_fits(int s, int n_max) {
   const int lda = frag_ld(round_up(s, 32));
-  const size_t d = round_up(3 * n_max + kP + 32, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) + (size_t)lda * n_max;
+  const size_t d = round_up(3 * n_max + kP + 34, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) + (size_t)lda * n_max;
   return n_max <= 16 * kP && d * sizeof(double) <= kMaxSmemBytes;
 }
 
 template <int MR>
 static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
   args.lda = frag_ld(round_up(args.s, 32));
-  const size_t d = round_up(3 * args.n_max + kP + 32, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
+  const size_t d = round_up(3 * args.n_max + kP + 34, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
                    (size_t)args.lda * args.n_max;
   const size_t smem = d * sizeof(double);
   cudaFuncSetAttribute(probe_fused_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
