@@ -10,7 +10,8 @@ import os
 
 from .errors import ConfigurationError, DimensionError, IllConditionedProbeError, NativeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_hbs_b200.so")
+# HBS_B200_LIB overrides the path (development builds of kernel variants)
+LIB_PATH = os.environ.get("HBS_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_hbs_b200.so")
 
 HBS_OK = 0
 HBS_ERR_DIMENSION = 1

@@ -86,6 +86,16 @@ HBS_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
 }
+// Same, with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing try_wait, leaving the
+// issue slots of its SM sub-partition to the warps doing the work.
+HBS_DEV void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity), "r"(1000000u) : "memory");
+}
 
 // Warp-uniform wait: one lane spins (acquire), then __syncwarp re-converges the
 // warp and orders the other lanes' later reads after the acquire.  Waiting in

@@ -29,7 +29,20 @@ __device__ int g_hqr_trace_mode = 0;   // record only kernels of this mode
 #define HQR_STEP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0) g_hqr_trace[64 + (i)] = clock64(); } while (0)
 #define FUSED_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0) g_hqr_trace[128 + (i)] = clock64(); } while (0)
 #define STEP_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 32 && lane == 0) g_hqr_trace[200 + (i)] = clock64(); } while (0)
+__device__ long long g_pf_trace[64];
+#define PF_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0 && lane == 0) g_pf_trace[8 * warp + (i)] = clock64(); } while (0)
+__device__ long long g_pf_step[64];
+#endif
+#if defined(HBS_TRACE) && defined(HBS_TRACE_STEP)
+// clock stamp once value v is available (warp 1 of the first panel only)
+#define PF_DEP(i, v) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0 && lane == 0 && warp == 1) { \
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(G + kP * kLdT - 1)), "d"(v) : "memory"); \
+    g_pf_step[8 * jl + (i)] = clock64(); } } while (0)
 #else
+#define PF_DEP(i, v) do { } while (0)
+#endif
+#ifndef HBS_TRACE
+#define PF_MARK(i) do { } while (0)
 #define FUSED_MARK(i) do { } while (0)
 #define STEP_MARK(i) do { } while (0)
 #define HQR_MARK(i) do { } while (0)
@@ -57,6 +70,43 @@ HBS_DEV Reflector make_reflector(double alpha, double xn2) {
     h.beta = -copysign(nrm, alpha);
     h.tau = fma(fabs(alpha), rho, 1.0);
     h.scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+  }
+  return h;
+}
+
+// make_reflector with the reciprocal square root and the reciprocal from
+// float seeds refined by two Newton steps in double (about a tenth of the
+// issue slots of the IEEE-exact library routines, which dominate a
+// single-warp panel step); the library path covers operands outside the
+// float seed's range.
+HBS_DEV double rsqrt_nr(double a) {
+#ifndef PF_EXP_NORANGE
+  if (!(a > 1e-30 && a < 1e30)) return rsqrt(a);
+#endif
+  double y = static_cast<double>(rsqrtf(static_cast<float>(a)));
+  const double ha = 0.5 * a;
+  y = y * fma(-ha * y, y, 1.5);
+  y = y * fma(-ha * y, y, 1.5);
+  return y;
+}
+HBS_DEV double rcp_nr(double a) {
+#ifndef PF_EXP_NORANGE
+  if (!(a > 1e-30 && a < 1e30)) return __drcp_rn(a);
+#endif
+  double y = static_cast<double>(__frcp_rn(static_cast<float>(a)));
+  y = fma(y, fma(-a, y, 1.0), y);
+  y = fma(y, fma(-a, y, 1.0), y);
+  return y;
+}
+HBS_DEV Reflector make_reflector_fast(double alpha, double xn2) {
+  Reflector h{0.0, alpha, 0.0};
+  if (xn2 != 0.0) {
+    const double s2 = fma(alpha, alpha, xn2);
+    const double rho = rsqrt_nr(s2);
+    const double nrm = s2 * rho;
+    h.beta = -copysign(nrm, alpha);
+    h.tau = fma(fabs(alpha), rho, 1.0);
+    h.scale = copysign(rcp_nr(fabs(alpha) + nrm), alpha);
   }
   return h;
 }
@@ -590,15 +640,20 @@ HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* 
         const int row = lane + 32 * k;
         x[c][k] = (cb + c < nbp && row < mr) ? A[(j0 + row) + (j0 + cb + c) * lda] : 0.0;
       }
+    PF_MARK(0);
     // reflectors 0 .. cb-1 (earlier warps), applied as they are published
     for (int j = 0; j < cb; ++j) {
+#ifdef PF_EXP_SLEEP
+      mbar_wait_sleep(&bar[j], parity);
+#else
       mbar_wait(&bar[j], parity);
+#endif
       const double tau = s_tau[j0 + j];
       double v[MR];
 #pragma unroll
       for (int k = 0; k < MR; ++k) {
         const int row = lane + 32 * k;
-        v[k] = (row > j && row < mr) ? A[(j0 + row) + (j0 + j) * lda] : (row == j ? 1.0 : 0.0);
+        v[k] = (k > 0 || row > j) ? (row < mr ? A[(j0 + row) + (j0 + j) * lda] : 0.0) : (row == j ? 1.0 : 0.0);
       }
       double pc[4];
 #pragma unroll
@@ -619,24 +674,50 @@ HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* 
         for (int k = 0; k < MR; ++k) x[c][k] = fma(-w, v[k], x[c][k]);
       }
     }
+    PF_MARK(1);
     // my first pivot: exact norm below row cb, alpha = row cb (lane cb, slot 0)
     double nrm, alpha;
     {
       double pp = 0.0;
 #pragma unroll
       for (int k = 0; k < MR; ++k)
-        if (lane + 32 * k > cb) pp = fma(x[0][k], x[0][k], pp);
+        if (k > 0 || lane > cb) pp = fma(x[0][k], x[0][k], pp);
       nrm = warp_sum(pp);
       alpha = __shfl_sync(0xffffffffu, x[0][0], cb);
     }
+    PF_MARK(2);
+    // publish column j: R above, beta on the diagonal, scaled tail below
+    auto publish = [&](int j, const Reflector& hh, const double (&xc)[MR]) {
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        if (row < mr) A[(j0 + row) + (j0 + j) * lda] = row < j ? xc[k] : (row == j ? hh.beta : xc[k] * hh.scale);
+      }
+      if (lane == 0) { s_tau[j0 + j] = hh.tau; s_scale[j0 + j] = hh.scale; s_beta[j0 + j] = hh.beta; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[j]);
+    };
+    Reflector hp{0.0, 0.0, 0.0};
+    double xp[MR];
+    int pubc = -1;
 #pragma unroll
     for (int jl = 0; jl < 4; ++jl) {
       const int j = cb + jl;
       if (j >= nbp) break;
+      PF_DEP(0, 0.0);
+#ifdef PF_EXP_NOREFL
+      const Reflector h{1.5 + 1e-300 * alpha, alpha, 0.5 + 1e-300 * nrm};
+#elif defined(PF_EXP_FASTREFL)
+      const Reflector h = make_reflector_fast(alpha, nrm);
+#else
       const Reflector h = make_reflector(alpha, nrm);
+#endif
+#ifndef PF_EXP_NOPUB
+      if (pubc >= 0) { publish(cb + pubc, hp, xp); pubc = -1; }
+#endif
       double pv[MR];
 #pragma unroll
-      for (int k = 0; k < MR; ++k) pv[k] = (lane + 32 * k > j) ? x[jl][k] : 0.0;
+      for (int k = 0; k < MR; ++k) pv[k] = (k > 0 || lane > j) ? x[jl][k] : 0.0;   // j < 32
       double pc[4] = {0.0, 0.0, 0.0, 0.0}, r[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int c = jl + 1; c < 4; ++c) {
@@ -654,11 +735,14 @@ HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* 
       if (jl < 3) {
 #pragma unroll
         for (int k = 0; k < MR; ++k)
-          if (lane + 32 * k > j + 1) { sxx = fma(x[jl + 1][k], x[jl + 1][k], sxx); spp = fma(pv[k], pv[k], spp); }
+          if (k > 0 || lane > j + 1) { sxx = fma(x[jl + 1][k], x[jl + 1][k], sxx); spp = fma(pv[k], pv[k], spp); }
         xn_old = __shfl_sync(0xffffffffu, x[jl + 1][0], j + 1);
         pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
       }
+      PF_DEP(1, pc[3] + r[3] + sxx + spp);
       const double dsum = reduce4_t(pc, lane);
+      PF_DEP(2, dsum);
+      PF_DEP(3, h.tau * h.scale);
       if (jl < 3) { sxx = warp_sum(sxx); spp = warp_sum(spp); }
       double gsn = 0.0, dn = 0.0;
 #pragma unroll
@@ -670,29 +754,37 @@ HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* 
         if (lane == j) x[c][0] -= f;
         if (c == jl + 1) { gsn = gs; dn = dc; }
       }
+      PF_DEP(4, x[3][0] + x[3][MR - 1]);
       if (jl < 3 && j + 1 < nbp) {
         // ||x'||^2 = sxx - 2 gs (x . pv) + gs^2 spp over rows > j+1
         double nn = fma(gsn * gsn, spp, fma(-2.0 * gsn, dn - pn * xn_old, sxx));
         alpha = fma(-gsn, pn, xn_old);
+#ifndef PF_EXP_NONEED
         if (!(nn > 0.5 * sxx) || sxx == 0.0) {   // warp-uniform
           double pp = 0.0;
 #pragma unroll
           for (int k = 0; k < MR; ++k)
-            if (lane + 32 * k > j + 1) pp = fma(x[jl + 1][k], x[jl + 1][k], pp);
+            if (k > 0 || lane > j + 1) pp = fma(x[jl + 1][k], x[jl + 1][k], pp);
           nn = warp_sum(pp);
         }
+#endif
         nrm = nn;
       }
-      // publish column j: R above, beta on the diagonal, scaled tail below
+      PF_DEP(5, nrm + alpha);
+      // column j is published at the top of the next step (after that
+      // step's reflector is issued) or after the loop
+#ifdef PF_EXP_DEFER
+      hp = h;
+      pubc = jl;
 #pragma unroll
-      for (int k = 0; k < MR; ++k) {
-        const int row = lane + 32 * k;
-        if (row < mr) A[(j0 + row) + (j0 + j) * lda] = row < j ? x[jl][k] : (row == j ? h.beta : x[jl][k] * h.scale);
-      }
-      if (lane == 0) { s_tau[j0 + j] = h.tau; s_scale[j0 + j] = h.scale; s_beta[j0 + j] = h.beta; }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar[j]);
+      for (int k = 0; k < MR; ++k) xp[k] = x[jl][k];
+#else
+      publish(j, h, x[jl]);
+#endif
+      PF_MARK(3 + jl);
+      PF_DEP(6, 0.0);
     }
+    if (pubc >= 0) publish(cb + pubc, hp, xp);
   }
   gsync<NTG>();
   panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
@@ -850,25 +942,36 @@ template <int NTG>
 HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G) {
   const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int kend = round_up(m, 4);
   for (int blk = warp; blk < 16; blk += nw) {
     const int fi = blk >> 2, fj = blk & 3;
     if (fi > fj) continue;  // only blocks on/above the diagonal are used
-    double c0 = 0.0, c1 = 0.0;
-    const int kend = round_up(m, 4);
-    for (int k = j0; k < kend; k += 4) {
+    // four independent accumulator chains (k-steps interleaved); rows above
+    // j0 + 8 fj are zero in column block fj
+    double c[4][2] = {};
+    int k = j0 + 8 * fj;
+    for (; k < j0 + kP && k < kend; k += 4) {
       const int i = k + t;
-      double av, bv;
-      if (k < j0 + kP) {
-        av = vval(A, lda, j0, nbp, i, 8 * fi + g);
-        bv = vval(A, lda, j0, nbp, i, 8 * fj + g);
-      } else {
-        av = (8 * fi + g < nbp) ? A[i + (j0 + 8 * fi + g) * lda] : 0.0;
-        bv = (8 * fj + g < nbp) ? A[i + (j0 + 8 * fj + g) * lda] : 0.0;
-      }
-      dmma8x8x4(c0, c1, av, bv);
+      dmma8x8x4(c[(k >> 2) & 3][0], c[(k >> 2) & 3][1], vval(A, lda, j0, nbp, i, 8 * fi + g),
+                vval(A, lda, j0, nbp, i, 8 * fj + g));
     }
-    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t] = c0;
-    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + 1] = c1;
+    const bool oki = 8 * fi + g < nbp, okj = 8 * fj + g < nbp;
+    const double* ci = A + (j0 + 8 * fi + g) * lda;
+    const double* cj = A + (j0 + 8 * fj + g) * lda;
+    for (; k < kend; k += 16) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = k + 4 * u + t;
+        const bool in = k + 4 * u < kend;
+        av[u] = (in && oki) ? ci[i] : 0.0;
+        bv[u] = (in && okj) ? cj[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma8x8x4(c[u][0], c[u][1], av[u], bv[u]);
+    }
+    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + 1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
   }
 }
 

@@ -2,6 +2,10 @@
 // in isolation, one CTA of 256 threads (pure latency) -- development tool.
 // Build: python gen_trace.py (writes pfq_trace.inc), then nvcc with the
 // library objects of paper_2205_02990_b200/csrc/build (see git log).
+#define HBS_TRACE
+#ifndef PB_NBP
+#define PB_NBP 32
+#endif
 #include "../../paper_2205_02990_b200/csrc/hqr.cu"
 #include "pfq_trace.inc"
 #include <cstdio>
@@ -30,7 +34,7 @@ __global__ void __launch_bounds__(256, 1) pf_bench(const double* Ain, int m, int
     }
     __syncthreads();
     const long long t0 = clock64();
-    panel_factor_r<6, 0>(A, lda, m, 0, kP, s_tau, s_scale, s_beta, bar, (unsigned)(r & 1), G);
+    panel_factor_r<6, 0>(A, lda, m, 0, PB_NBP, s_tau, s_scale, s_beta, bar, (unsigned)(r & 1), G);
     __syncthreads();
     tot += clock64() - t0;
   }
@@ -95,5 +99,27 @@ int main() {
     printf("\n");
   }
   printf("avg:"); for (int k = 0; k < 10; ++k) printf(" %s %.0f", k ? nm[k] : "handoff", acc[k] / (k ? 30 : 29)); printf("\n");
+  {
+    long long pt[64];
+    hbs::pf_bench<<<1, 256, smem>>>(d, m, 1, o);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(pt, hbs::g_pf_trace, sizeof(pt));
+    long long t0 = pt[0];
+    for (int w = 0; w < 8; ++w) t0 = pt[8 * w] < t0 ? pt[8 * w] : t0;
+    for (int w = 0; w < 8; ++w) {
+      printf("warp %d: loaded %6lld phase1 %6lld norm %6lld steps", w, pt[8 * w] - t0, pt[8 * w + 1] - t0, pt[8 * w + 2] - t0);
+      for (int jl = 0; jl < 4; ++jl) printf(" %6lld", pt[8 * w + 3 + jl] - t0);
+      printf("\n");
+    }
+    long long ps[64];
+    cudaMemcpyFromSymbol(ps, hbs::g_pf_step, sizeof(ps));
+    const char* nm[7] = {"start", "dots", "reduce", "refl", "update", "nrm", "publish"};
+    for (int jl = 0; jl < 4; ++jl) {
+      printf("warp 1 step %d:", jl);
+      for (int i = 1; i < 7; ++i) printf(" %s %5lld", nm[i], ps[8 * jl + i] - ps[8 * jl + i - 1]);
+      if (jl < 3) printf(" | next %5lld", ps[8 * (jl + 1)] - ps[8 * jl + 6]);
+      printf("\n");
+    }
+  }
   return 0;
 }
