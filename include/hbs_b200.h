@@ -113,6 +113,16 @@ int hbs_basis_qr_scratch_bytes(int64_t nbox, int max_rows, int r, size_t* bytes)
 int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
                  const double* b, double* q, double* scratch, void* stream);
 
+/* Building block: the orthonormal bases hbs_compress_level uses for col()
+ * (linalg.py:35-49): CholeskyQR2 on the FP64 tensor cores, any orthonormal
+ * basis of span(b) (the reference's result only depends on the span, see
+ * cholqr.cu), with the Householder kernel re-run for blocks whose Cholesky
+ * breaks down (rank-deficient, zero, or condition number beyond ~1e6).
+ * flags: nbox int32 scratch; on return flags[b] = 1 where the fallback ran.
+ * Needs max_rows <= 128 and r <= 64, else HBS_ERR_UNSUPPORTED. */
+int hbs_basis_orth(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
+                   const double* b, double* q, int32_t* flags, double* scratch, void* stream);
+
 /* Number of CUDA kernels launched by this library so far (process-wide). */
 unsigned long long hbs_launch_counter(void);
 

@@ -59,6 +59,7 @@ struct LevelWs {
   double* P[2];   // Y P and Z Q
   double* G1; double* M3; double* M4; double* E1; double* E2;
   double* gscratch;
+  int32_t* qr_flag;   // 2 x nbox CholeskyQR2 breakdown flags
   bool fused;
   // where the solve results live after factor_and_solve
   const double* Xp[2]; int ldX; int64_t strideX;   // Y Omega^+ / Z Psi^+
@@ -87,8 +88,10 @@ size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bo
     w.M4 = c.take<double>(nb * r * nr);
     w.E1 = c.take<double>(nb * r * nr);
     w.E2 = c.take<double>(nb * r * nr);
+    w.qr_flag = c.take<int32_t>(2 * nb);
   } else {
     w.G1 = w.M3 = w.M4 = w.E1 = w.E2 = nullptr;
+    w.qr_flag = nullptr;
   }
   const bool big_factor = !hqr_fits_smem(s, nr, kGeqrfFactor);
   const bool big_ortho = !root_only && !hqr_fits_smem(nr, r, kGeqrfOrtho);
@@ -248,6 +251,11 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     S.src = w.Pp[sd]; S.src_c_rb = 0; S.src_c_b = w.strideP; S.src_rs = w.ldP; S.src_cs = 1;
     S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
+  if (cholqr_fits(nr, r)) {
+    // CholeskyQR2 on the tensor cores; Householder only for flagged blocks
+    HBS_TRY(launch_cholqr(g, 2, w.qr_flag, st));
+    g.only = w.qr_flag;
+  }
   HBS_TRY(launch_hqr(g, 2, st));
   g_timer.mark();
 
@@ -351,6 +359,24 @@ int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, 
     S.q = q; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
   return launch_hqr(g, 1, static_cast<cudaStream_t>(stream));
+}
+
+int hbs_basis_orth(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
+                   const double* b, double* q, int32_t* flags, double* scratch, void* stream) {
+  if (nbox < 1 || max_rows < r || r < 1 || !flags) return HBS_ERR_DIMENSION;
+  if (!cholqr_fits(max_rows, r)) return HBS_ERR_UNSUPPORTED;
+  GeqrfArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.geo = LevelGeo{row_begin, sq_off, nbox}; g.mode = kGeqrfOrtho;
+  g.m_fixed = 0; g.m_is_rows = 1; g.n_fixed = r; g.n_is_rows = 0;
+  g.m_max = max_rows; g.n_max = r; g.gscratch = scratch;
+  GeqrfSide& S = g.side[0];
+  S.src = b; S.src_c_rb = r; S.src_c_b = 0; S.src_rs = r; S.src_cs = 1;
+  S.q = q; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HBS_TRY(launch_cholqr(g, 1, flags, st));
+  g.only = flags;
+  return launch_hqr(g, 1, st);
 }
 
 int hbs_basis_qr_scratch_bytes(int64_t nbox, int max_rows, int r, size_t* bytes) {

@@ -52,6 +52,7 @@ struct GeqrfArgs {
   double tol;
   double* gscratch;  // needed when the matrix does not fit in shared memory
   int use_smem;
+  const int32_t* only;  // if set: process (box b, side) only when only[side*nbox + b] != 0
 };
 
 // Blocked Householder (hqr.cu): kFactor also emits the per-panel T and R
@@ -60,6 +61,13 @@ size_t hqr_smem_bytes(int m_max, int n_max, int mode, bool with_matrix);
 size_t hqr_scratch_doubles(int m_max, int n_max, int64_t nbox);
 bool hqr_fits_smem(int m_max, int n_max, int mode);
 int launch_hqr(GeqrfArgs args, int nsides, cudaStream_t stream);
+
+// ---------------------------------------------------------------- CholeskyQR2 bases
+// Orthonormal basis of each box's (rows x r) block (GeqrfArgs in kOrtho form:
+// side[].src/q addressing, n_fixed = r, m_max = max rows).  flag[side*nbox + b]
+// = 1 marks a breakdown; those blocks go to launch_hqr with only = flag.
+bool cholqr_fits(int n_max, int r);
+int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream);
 
 // ---------------------------------------------------------------- fused probe QR + apply Q + solve
 // Per (box, side): Householder QR of Omega_tau^T in shared memory (warps 0-7)

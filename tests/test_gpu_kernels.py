@@ -133,3 +133,57 @@ def test_basis_qr_matches_lapack(rows, r):
         if np.linalg.matrix_rank(b) == r:
             assert np.abs(q - q_ref).max() <= 1e-11      # same reflectors => same Q (LAPACK signs)
         assert np.linalg.norm(b - q @ (q.T @ b)) <= 1e-12 * max(1.0, np.linalg.norm(b))
+
+
+def basis_orth(blocks, r):
+    rows = [b.shape[0] for b in blocks]
+    nr = max(rows)
+    begins = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    sq = np.concatenate([[0], np.cumsum(np.array(rows) ** 2)]).astype(np.int64)
+    dev = torch.device("cuda")
+    bb = torch.from_numpy(np.concatenate(blocks)).to(dev)
+    q = torch.zeros_like(bb)
+    rb, so = torch.from_numpy(begins).to(dev), torch.from_numpy(sq).to(dev)
+    flags = torch.zeros(len(blocks), dtype=torch.int32, device=dev)
+    sz = ctypes.c_size_t()
+    _native.check(_native.lib().hbs_basis_qr_scratch_bytes(len(blocks), nr, r, ctypes.byref(sz)), "scratch")
+    scratch = torch.empty(max(sz.value // 8, 1), dtype=torch.float64, device=dev)
+    rc = _native.lib().hbs_basis_orth(len(blocks), rb.data_ptr(), so.data_ptr(), nr, r, bb.data_ptr(), q.data_ptr(),
+                                      flags.data_ptr(), scratch.data_ptr() if sz.value else 0,
+                                      torch.cuda.current_stream().cuda_stream)
+    _native.check(rc, "hbs_basis_orth")
+    torch.cuda.synchronize()
+    qh = q.cpu().numpy()
+    return [qh[begins[j]:begins[j + 1]] for j in range(len(blocks))], flags.cpu().numpy()
+
+
+@pytest.mark.parametrize("rows,r", [(128, 64), (32, 16), (64, 32), (80, 40), (21, 8), (120, 40), (40, 40), (96, 48)])
+def test_basis_orth_cholqr2(rows, r):
+    """CholeskyQR2 bases (cholqr.cu): orthonormal, same span as the reference's
+    col() (linalg.py:35-49), hence the same projector as LAPACK's Q; the
+    Householder kernel takes over for rank-deficient / very ill-conditioned blocks."""
+    rng = np.random.default_rng(rows * 1000 + r)
+    blocks = [rng.standard_normal((rows, r)) for _ in range(3)]
+    u, _, vt = np.linalg.svd(rng.standard_normal((rows, r)), full_matrices=False)
+    blocks.append((u * np.logspace(0, -5, r)) @ vt)          # kappa 1e5: second full Cholesky pass
+    blocks.append(np.zeros((rows, r)))                       # breakdown -> Householder
+    blocks.append(rng.standard_normal((rows, 2)) @ rng.standard_normal((2, r)))   # rank 2 -> Householder
+    blocks.append((u * np.logspace(0, -9, r)) @ vt)          # kappa 1e9 -> Householder
+    qs, flags = basis_orth(blocks, r)
+    assert list(flags[:4]) == [0, 0, 0, 0] and list(flags[4:]) == [1, 1, 1]
+    for j, (b, q) in enumerate(zip(blocks, qs)):
+        assert np.linalg.norm(q.T @ q - np.eye(r)) <= 1e-13 * r, j
+        assert np.linalg.norm(b - q @ (q.T @ b)) <= 1e-13 * max(1.0, np.linalg.norm(b)), j
+        if j < 4:
+            q_ref = np.linalg.qr(b)[0]
+            assert np.linalg.norm(q @ q.T - q_ref @ q_ref.T) <= 1e-12 * (1e5 if j == 3 else 1.0), j
+
+
+def test_basis_orth_uneven_rows():
+    rng = np.random.default_rng(11)
+    blocks = [rng.standard_normal((n, 24)) for n in (24, 57, 128, 96, 31)]
+    qs, flags = basis_orth(blocks, 24)
+    assert not flags.any()
+    for b, q in zip(blocks, qs):
+        assert np.linalg.norm(q.T @ q - np.eye(24)) <= 1e-13 * 24
+        assert np.linalg.norm(b - q @ (q.T @ b)) <= 1e-13 * np.linalg.norm(b)

@@ -21,7 +21,7 @@ lib.hbs_compress_level(g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.ma
                        *(m.data_ptr() for m in out), plan.workspace.data_ptr(), plan.workspace_bytes,
                        plan.status.data_ptr(), 0)
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * 256)()
+buf = (ctypes.c_longlong * 320)()
 getattr(lib, "hbs_debug_hqr_trace")(buf)
 t = list(buf)
 f = t[128:128 + 48]
@@ -43,3 +43,8 @@ sp = t[64 + 40: 64 + 56]
 for q in range(4):
     a = sp[4 * q: 4 * q + 4]
     print(f"sub {q}: end-of-steps->finalised {a[1]-a[0]}  W partial {a[2]-a[1]}  W'+update {a[3]-a[2]}  (steps start {st[8*q]-t[2]})")
+pf = t[256:320]
+base = f[0]
+print("panel-factor per-warp marks (cycles from fused start; 0 start, 1 earlier reflectors applied, 2 first norm, 3..6 own steps):")
+for w in range(8):
+    print(f"  warp {w}:", [pf[8 * w + i] - base if pf[8 * w + i] else None for i in range(7)])
