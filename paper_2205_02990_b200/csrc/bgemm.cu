@@ -1,20 +1,26 @@
 // Batched, variable-size fp64 GEMM on the FP64 tensor cores (DMMA m8n8k4),
-// one launch per level-wide product (box b = blockIdx.z):
+// one launch per level-wide product (box b = tile group of blockIdx.x):
 //     C_b = alpha * op(A_b) op(B_b) + beta * C0_b
 // Operand bases are derived from the level geometry (row starts, packed
 // square-block offsets), so the same kernel serves the discrepancy algebra
 // (compress.py:192-197), the parent-sample lift (compress.py:209-227) and the
 // telescoping apply used by the HBS sampler (factorization.py:89-143).
-// 64 x 64 CTA tile, BK = 16, cp.async double buffering, 8 warps of 32 x 16.
+//
+// 64 x 64 CTA tile, 4 warps of 32 x 32 (16 MMAs per 8 fragment loads per
+// k-step), BK = 16, 3-stage cp.async pipeline (3 CTAs per SM) with 16-byte
+// copies when every operand row start of the box is 16-byte aligned.  Each operand is staged in the
+// orientation it has in global memory (contiguous runs stay contiguous), and
+// both staging layouts give bank-conflict-free m8n8k4 fragment loads.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace hbs {
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16;
-constexpr int LDA_S = 20;  // BK + 4  (== 4 mod 16)
-constexpr int LDB_S = 68;  // BN + 4
+constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3, NT = 128;
+constexpr int LDK = BK + 4;   // k-contiguous staging: [row][k]  (== 4 mod 16)
+constexpr int LDR = BM + 4;   // row-contiguous staging: [k][row]
+constexpr int STAGE = BM * LDK > BK * LDR ? BM * LDK : BK * LDR;   // doubles per operand stage
 
 HBS_DEV int64_t op_off(const BOperand& o, const LevelGeo& g, int64_t b) {
   int64_t off = o.c_b * b;
@@ -23,11 +29,66 @@ HBS_DEV int64_t op_off(const BOperand& o, const LevelGeo& g, int64_t b) {
   return off;
 }
 
+HBS_DEV void cp_async16(double* dst, const double* src, int bytes) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src), "r"(bytes));
+}
+
+// Stage a 64 x 16 (rows x k) operand tile whose global element (i, k) sits at
+// p[i * ld + k] (KC = true: k contiguous) or p[k * ld + i] (KC = false).
+// KC: smem [i][k] (ld LDK); else smem [k][i] (ld LDR).
+template <bool KC>
+HBS_DEV void stage_tile(double* s, const double* p, int ld, int i0, int k0, int I, int K, int tid, bool vec) {
+  if (vec) {
+#pragma unroll
+    for (int e = 0; e < (BM * BK / 2) / NT; ++e) {
+      const int idx = tid + e * NT;
+      int i, k;
+      if (KC) { i = idx >> 3; k = 2 * (idx & 7); }
+      else { k = idx >> 5; i = 2 * (idx & 31); }
+      const int gi = i0 + i, gk = k0 + k;
+      int bytes;
+      const double* src;
+      if (KC) {
+        bytes = (gi < I && gk < K) ? (gk + 1 < K ? 16 : 8) : 0;
+        src = p + (int64_t)gi * ld + gk;
+      } else {
+        bytes = (gi < I && gk < K) ? (gi + 1 < I ? 16 : 8) : 0;
+        src = p + (int64_t)gk * ld + gi;
+      }
+      cp_async16(KC ? &s[i * LDK + k] : &s[k * LDR + i], bytes ? src : p, bytes);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < (BM * BK) / NT; ++e) {
+      const int idx = tid + e * NT;
+      int i, k;
+      if (KC) { i = idx >> 4; k = idx & 15; }
+      else { k = idx >> 6; i = idx & 63; }
+      const int gi = i0 + i, gk = k0 + k;
+      const bool ok = gi < I && gk < K;
+      const double* src = KC ? p + (int64_t)gi * ld + gk : p + (int64_t)gk * ld + gi;
+      cp_async8(KC ? &s[i * LDK + k] : &s[k * LDR + i], ok ? src : p, ok);
+    }
+  }
+}
+
+// fragment element (row, k) of a staged tile
+template <bool KC>
+HBS_DEV double frag(const double* s, int row, int k) {
+  return KC ? s[row * LDK + k] : s[k * LDR + row];
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(256) bgemm_kernel(BgemmArgs args) {
-  __shared__ __align__(16) double As[2][BM * LDA_S];
-  __shared__ __align__(16) double Bs[2][BK * LDB_S];
+// A(i, k): trans = 0 -> A[i*lda + k] (k contiguous); B(k, j): trans = 1 -> B[j*ldb + k] (k contiguous).
+HBS_DEV bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <bool AKC, bool BKC>
+__global__ void __launch_bounds__(NT, 3) bgemm_kernel(BgemmArgs args) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                       // NSTAGE x STAGE
+  double* Bs = smem + NSTAGE * STAGE;      // NSTAGE x STAGE
   // blockIdx.x = box * (tiles_m * tiles_n) + tile: a box's tiles run back to back (L2 reuse)
   const int tn_max = (args.N_max + BN - 1) / BN, tm_max = (args.M_max + BM - 1) / BM;
   const int64_t b = blockIdx.x / (tm_max * tn_max);
@@ -43,64 +104,48 @@ __global__ void __launch_bounds__(256) bgemm_kernel(BgemmArgs args) {
   const double* A = args.A.p + op_off(args.A, args.geo, b);
   const double* B = args.B.p + op_off(args.B, args.geo, b);
   const int tid = threadIdx.x;
+  // 16-byte staging when every row start of this box's operands is aligned
+  const bool vec = al16(A) && al16(B) && (lda % 2 == 0) && (ldb % 2 == 0);
 
-  auto load_tile = [&](int buf, int k0) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = tid + e * 256;
-      int i, k;
-      if (!args.A.trans) { i = idx >> 4; k = idx & 15; }
-      else { i = idx & 63; k = idx >> 6; }
-      const bool ok = (m0 + i < M) && (k0 + k < K);
-      const double* src = args.A.trans ? A + (int64_t)(k0 + k) * lda + (m0 + i)
-                                       : A + (int64_t)(m0 + i) * lda + (k0 + k);
-      cp_async8(&As[buf][i * LDA_S + k], ok ? src : A, ok);
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = tid + e * 256;
-      int k, j;
-      if (!args.B.trans) { k = idx >> 6; j = idx & 63; }
-      else { j = idx >> 4; k = idx & 15; }
-      const bool ok = (k0 + k < K) && (n0 + j < N);
-      const double* src = args.B.trans ? B + (int64_t)(n0 + j) * ldb + (k0 + k)
-                                       : B + (int64_t)(k0 + k) * ldb + (n0 + j);
-      cp_async8(&Bs[buf][k * LDB_S + j], ok ? src : B, ok);
-    }
-    cp_async_commit();
+  auto load = [&](int stage, int k0) {
+    stage_tile<AKC>(As + stage * STAGE, A, lda, m0, k0, M, K, tid, vec);
+    stage_tile<BKC>(Bs + stage * STAGE, B, ldb, n0, k0, N, K, tid, vec);
   };
 
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;   // 2 x 4 warps, warp tile 32 x 16
-  double acc[4][2][2] = {};
+  const int wm = warp >> 1, wn = warp & 1;   // 2 x 2 warps, warp tile 32 x 32
+  double acc[4][4][2] = {};
   const int nk = (K + BK - 1) / BK;
-  if (nk > 0) load_tile(0, 0);
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nk) load(s, s * BK);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) {
-      load_tile(buf ^ 1, (kt + 1) * BK);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<NSTAGE - 2>();
     __syncthreads();
-    const double* as = As[buf];
-    const double* bs = Bs[buf];
+    {   // refill the stage consumed last iteration
+      const int kn = kt + NSTAGE - 1;
+      if (kn < nk) load(kn % NSTAGE, kn * BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % NSTAGE) * STAGE;
+    const double* bs = Bs + (kt % NSTAGE) * STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[2];
+      double af[4], bf[4];
 #pragma unroll
-      for (int fi = 0; fi < 4; ++fi) af[fi] = as[(wm * 32 + fi * 8 + g) * LDA_S + kk + t];
+      for (int fi = 0; fi < 4; ++fi) af[fi] = frag<AKC>(as, wm * 32 + fi * 8 + g, kk + t);
 #pragma unroll
-      for (int fj = 0; fj < 2; ++fj) bf[fj] = bs[(kk + t) * LDB_S + wn * 16 + fj * 8 + g];
+      for (int fj = 0; fj < 4; ++fj) bf[fj] = frag<BKC>(bs, wn * 32 + fj * 8 + g, kk + t);
 #pragma unroll
       for (int fi = 0; fi < 4; ++fi)
 #pragma unroll
-        for (int fj = 0; fj < 2; ++fj) dmma8x8x4(acc[fi][fj][0], acc[fi][fj][1], af[fi], bf[fj]);
+        for (int fj = 0; fj < 4; ++fj) dmma8x8x4(acc[fi][fj][0], acc[fi][fj][1], af[fi], bf[fj]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   const int ldc = args.ldc_rows ? rows : args.ldc_fixed;
   double* C = args.C + args.cc_b * b + (args.cc_rb ? args.cc_rb * args.geo.row_begin[b] : 0) +
@@ -108,33 +153,57 @@ __global__ void __launch_bounds__(256) bgemm_kernel(BgemmArgs args) {
   const bool has_c0 = args.beta != 0.0;
   const int ldc0 = args.C0.ld_rows ? rows : args.C0.ld_fixed;
   const double* C0 = has_c0 ? args.C0.p + op_off(args.C0, args.geo, b) : nullptr;
+  const bool cvec = al16(C) && (ldc % 2 == 0);
 #pragma unroll
   for (int fi = 0; fi < 4; ++fi)
 #pragma unroll
-    for (int fj = 0; fj < 2; ++fj)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = m0 + wm * 32 + fi * 8 + g;
-        const int j = n0 + wn * 16 + fj * 8 + 2 * t + e;
-        if (i < M && j < N) {
-          double v = args.alpha * acc[fi][fj][e];
-          if (has_c0) {
-            const double c0 = args.C0.trans ? C0[(int64_t)j * ldc0 + i] : C0[(int64_t)i * ldc0 + j];
-            v = fma(args.beta, c0, v);
-          }
-          C[(int64_t)i * ldc + j] = v;
+    for (int fj = 0; fj < 4; ++fj) {
+      const int i = m0 + wm * 32 + fi * 8 + g;
+      const int j = n0 + wn * 32 + fj * 8 + 2 * t;
+      if (i >= M) continue;
+      double v0 = args.alpha * acc[fi][fj][0], v1 = args.alpha * acc[fi][fj][1];
+      if (has_c0) {
+        if (args.C0.trans) {
+          if (j < N) v0 = fma(args.beta, C0[(int64_t)j * ldc0 + i], v0);
+          if (j + 1 < N) v1 = fma(args.beta, C0[(int64_t)(j + 1) * ldc0 + i], v1);
+        } else {
+          if (j < N) v0 = fma(args.beta, C0[(int64_t)i * ldc0 + j], v0);
+          if (j + 1 < N) v1 = fma(args.beta, C0[(int64_t)i * ldc0 + j + 1], v1);
         }
       }
+      double* cp = C + (int64_t)i * ldc + j;
+      if (cvec && j + 1 < N) {
+        *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+      } else {
+        if (j < N) cp[0] = v0;
+        if (j + 1 < N) cp[1] = v1;
+      }
+    }
 }
+
+namespace {
+
+template <bool AKC, bool BKC>
+int launch_t(const BgemmArgs& args, dim3 grid, cudaStream_t stream) {
+  const size_t smem = 2 * NSTAGE * STAGE * sizeof(double);
+  cudaFuncSetAttribute(bgemm_kernel<AKC, BKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bgemm_kernel<AKC, BKC><<<grid, NT, smem, stream>>>(args);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+}  // namespace
 
 int launch_bgemm(const BgemmArgs& args, cudaStream_t stream) {
   if (args.geo.nbox <= 0 || args.M_max <= 0 || args.N_max <= 0) return kOk;
   const int64_t tiles = (int64_t)((args.N_max + BN - 1) / BN) * ((args.M_max + BM - 1) / BM);
   if (tiles * args.geo.nbox >= (1ll << 31)) return kErrUnsupported;
   dim3 grid((unsigned)(tiles * args.geo.nbox));
-  bgemm_kernel<<<grid, 256, 0, stream>>>(args);
   note_launch();
-  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+  const bool akc = !args.A.trans, bkc = args.B.trans != 0;
+  if (akc && bkc) return launch_t<true, true>(args, grid, stream);
+  if (akc) return launch_t<true, false>(args, grid, stream);
+  if (bkc) return launch_t<false, true>(args, grid, stream);
+  return launch_t<false, false>(args, grid, stream);
 }
 
 }  // namespace hbs

@@ -274,18 +274,18 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Wt, w.G1, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
   HBS_TRY(gemm(geo, dfix(r), dfix(r), drows(), r, r, G1, Vn, w.M3, 0, (int64_t)r * r, 0, r, false, 1.0, 0.0,
                none, st));
-  HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Xn, w.M4, 0, rs, 0, nr, false, 1.0, -1.0, G1, st));
-  HBS_TRY(gemm(geo, dfix(r), drows(), dfix(r), r, nr, M3, Vt, w.M4, 0, rs, 0, nr, false, 1.0, 1.0, M4, st));
+  // E1 = G1 - M3 V^T (= U^T D, reused by the lift), M4 = U^T X - E1
+  const BOperand E1 = op(w.E1, 0, rs, 0, nr, false, false);
+  HBS_TRY(gemm(geo, dfix(r), drows(), dfix(r), r, nr, M3, Vt, w.E1, 0, rs, 0, nr, false, -1.0, 1.0, G1, st));
+  HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Xn, w.M4, 0, rs, 0, nr, false, 1.0, -1.0, E1, st));
   HBS_TRY(gemm(geo, drows(), drows(), dfix(r), nr, nr, Un, M4, d, 0, 0, 1, 0, true, -1.0, 1.0, Xn, st));
   g_timer.mark();
 
   if (lift_omega) {
     // Parent quadruple rows of child b: [b*r, (b+1)*r)  (compress.py:209-227)
-    const BOperand Dn = op(d, 0, 0, 1, 0, true, false);
     const BOperand Dt = op(d, 0, 0, 1, 0, true, true);
-    const BOperand E1 = op(w.E1, 0, rs, 0, nr, false, false);
+    // U^T D = E1 from the discrepancy algebra (U^T U = I); V^T D^T directly
     const BOperand E2 = op(w.E2, 0, rs, 0, nr, false, false);
-    HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Dn, w.E1, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
     HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Vt, Dt, w.E2, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
     const BOperand Om = op(omega, s, 0, 0, s, false, false);
     const BOperand Ps = op(psi, s, 0, 0, s, false, false);

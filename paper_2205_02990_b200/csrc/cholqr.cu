@@ -34,6 +34,18 @@ constexpr int kNmax = 128;          // max rows per box
 
 HBS_DEV void csync() { __syncthreads(); }
 
+// 1/sqrt(a) from the float estimate and two Newton steps in double (the
+// library routine's special-case handling dominates a Cholesky step); the
+// library covers operands outside the float range.
+HBS_DEV double rsqrt_fast(double a) {
+  if (!(a > 1e-30 && a < 1e30)) return rsqrt(a);
+  double y = static_cast<double>(rsqrtf(static_cast<float>(a)));
+  const double ha = 0.5 * a;
+  y = y * fma(-ha * y, y, 1.5);
+  y = y * fma(-ha * y, y, 1.5);
+  return y;
+}
+
 // G(0:rp, 0:rp) = A^T A for A (npad x rp, row-major, ld lda) on the tensor
 // cores; G column-major (G(i, j) at G[i + j*kLdG]); only blocks bi <= bj
 // (diagonal blocks in full).
@@ -74,7 +86,7 @@ __device__ __noinline__ bool chol16(double* G, int o, const double* gdiag, doubl
   for (int j = 0; j < 16; ++j) {
     const double d = __shfl_sync(0xffffffffu, c[j], j);
     ok = ok && (d > 1e-12 * gdiag[o + j]) && (d < INFINITY);
-    const double rs = rsqrt(d);
+    const double rs = rsqrt_fast(d);
     if (kc == j) c[j] = d * rs;
     else if (kc > j) c[j] *= rs;
     else c[j] = 0.0;
@@ -320,16 +332,36 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
   double* rowbuf = rdinv + kRc;           // 32 (Cholesky row broadcast)
   int* s_ok = reinterpret_cast<int*>(rowbuf + 32);
   double* s_e2 = rowbuf + 33;
-  double* A = rowbuf + 34;                // npad x lda
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(rowbuf + 34);
+  double* A = rowbuf + 36;                // npad x lda (16-byte aligned rows)
   int32_t* myflag = flag + (int64_t)side * args.geo.nbox + b;
 
   const int64_t rb = args.geo.row_begin[b];
   const double* src = S.src + S.src_c_rb * rb + S.src_c_b * b;
-  for (int e = threadIdx.x; e < npad * rc; e += kCT) {
-    const int i = e / rc, j = e - i * rc;
-    A[i * lda + j] = (i < nb && j < r) ? __ldcg(src + i * S.src_rs + j * S.src_cs) : 0.0;
+  // rows are contiguous r-double runs: one TMA bulk copy per row when aligned
+  const bool bulk = S.src_cs == 1 && (r & 1) == 0 && (S.src_rs & 1) == 0 &&
+                    (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    csync();
+    if (threadIdx.x == 0) mbar_expect_tx(s_bar, (unsigned)(nb * r * sizeof(double)));
+    csync();
+    for (int i = threadIdx.x; i < nb; i += kCT) bulk_g2s(&A[i * lda], src + i * S.src_rs, (unsigned)(r * sizeof(double)), s_bar);
+    for (int e = threadIdx.x; e < npad * rc; e += kCT) {
+      const int i = e / rc, j = e - i * rc;
+      if (i >= nb || j >= r) A[i * lda + j] = 0.0;
+    }
+  } else {
+    for (int e = threadIdx.x; e < npad * rc; e += kCT) {
+      const int i = e / rc, j = e - i * rc;
+      A[i * lda + j] = (i < nb && j < r) ? __ldcg(src + i * S.src_rs + j * S.src_cs) : 0.0;
+    }
   }
   for (int e = threadIdx.x; e < kRc * kLdG; e += kCT) G[e] = 0.0;
+  if (bulk) mbar_wait(s_bar, 0);
   csync();
 
   bool fail = nb < r;
@@ -390,7 +422,7 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
 bool cholqr_fits(int n_max, int r) { return n_max <= kNmax && r <= kRc && r >= 1; }
 
 size_t cholqr_smem_bytes(int n_max, int r) {
-  return ((size_t)kRc * kLdG + 2 * kRc + 34 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
+  return ((size_t)kRc * kLdG + 2 * kRc + 36 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
 }
 
 int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream) {
