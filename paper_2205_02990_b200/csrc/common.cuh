@@ -140,4 +140,54 @@ HBS_DEV double cfrag_to_afrag(const double (&acc)[NF][2], int kk, int lane) {
   return (col & 1) ? v1 : v0;
 }
 
+// ---------------------------------------------------------------- TMEM (tcgen05) as an fp64 scratchpad
+// fp64 element (lane i, column c) occupies 32-bit TMEM columns 2c (low word)
+// and 2c + 1 (high word).  A .16x256b access by a warp covers 16 lanes
+// (rows) x 4 fp64 columns per repetition; thread (g = lane/4, t = lane%4)
+// holds (row g, col c0 + t) and (row g + 8, col c0 + t) -- the m8n8k4
+// A-fragment layout of two 8-row groups.  Warp w may only touch lanes
+// 32 (w % 4) .. 32 (w % 4) + 31.
+HBS_DEV void tm_alloc512(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+      static_cast<unsigned>(__cvta_generic_to_shared(slot))));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+HBS_DEV void tm_dealloc512(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
+}
+HBS_DEV void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+HBS_DEV void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+HBS_DEV void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// 16 columns (4 repetitions): v[rep][h] = (row g + 8h, col c0 + 4 rep + t)
+HBS_DEV void tm_ld16(uint32_t taddr, double (&v)[4][2]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[q][0] = __hiloint2double((int)r[4 * q + 1], (int)r[4 * q + 0]);
+    v[q][1] = __hiloint2double((int)r[4 * q + 3], (int)r[4 * q + 2]);
+  }
+}
+HBS_DEV void tm_st16(uint32_t taddr, const double (&v)[4][2]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    r[4 * q + 0] = (uint32_t)__double2loint(v[q][0]);
+    r[4 * q + 1] = (uint32_t)__double2hiint(v[q][0]);
+    r[4 * q + 2] = (uint32_t)__double2loint(v[q][1]);
+    r[4 * q + 3] = (uint32_t)__double2hiint(v[q][1]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
 }  // namespace hbs

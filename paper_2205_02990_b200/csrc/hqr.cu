@@ -1382,7 +1382,11 @@ HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* ou
 
 }  // namespace
 
-template <int MR>
+// TM: the box's Y rows live in tensor memory for the whole sweep (n_max <=
+// 128 rows -> TMEM lanes, s <= 256 fp64 columns), so the Y group's three
+// products per panel and the solve read and write Y there instead of
+// round-tripping it through L2.
+template <int MR, bool TM>
 __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   extern __shared__ double smem[];
   const int side = blockIdx.y;
@@ -1402,10 +1406,11 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   double* s_beta = s_scale + args.n_max;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + args.n_max);   // 32 step barriers
   uint64_t* s_ready = s_bar + kP;                                          // 16 panel-ready + 1 R-ready
-  double* G = smem + round_up(3 * args.n_max + kP + 34, 2);
+  double* G = smem + round_up(3 * args.n_max + kP + 35, 2);
   double* Tscr = G + kP * kLdT;
   double* T = Tscr + 384;
   double* A = T + round_up(kP * kLdT, 2);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_ready + 34);
 
   // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1.
   // Each column is one contiguous Omega row: TMA bulk copies (one per column)
@@ -1416,7 +1421,10 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
                     ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   if (threadIdx.x < kP + 34) mbar_init(&s_bar[threadIdx.x], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  if (TM && warp == 0) tm_alloc512(s_tmem);
+  tm_fence_before();
   __syncthreads();
+  tm_fence_after();
   if (bulk) {
     if (threadIdx.x == 0) mbar_expect_tx(s_load, (unsigned)(n * m * sizeof(double)));
     __syncthreads();
@@ -1537,6 +1545,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         FUSED_MARK(20);
       }
     }
+    if constexpr (TM) return;   // the solve runs on the TMEM-resident rows (group Y)
     // group Y has applied every panel and inverted every diagonal block of R:
     // take row groups lt/32 (mod 16) of the solve
     mbar_wait(&s_ready[32], 0);
@@ -1546,6 +1555,194 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
 
   // -------------------------------------------------------------- group Y
   const int yw = warp;   // group Y: physical warps 0..7
+  if constexpr (TM) {
+    // warp yw owns rows R0 .. R0+15 (TMEM lanes of its quadrant); thread
+    // (g, t) holds rows R0 + g and R0 + 8 + g.  C-fragments of an 8-column
+    // block n0 are kept column-permuted: position 2t <-> column n0 + t,
+    // 2t + 1 <-> n0 + 4 + t, i.e. sigma(j) = j/2 + 4 (j & 1).
+    const uint32_t tbase = *s_tmem;
+    const int R0 = 32 * (yw & 3) + 16 * (yw >> 2);
+    const uint32_t tl = tbase + ((uint32_t)R0 << 16);
+    const int rowh[2] = {R0 + g, R0 + 8 + g};
+    const bool okh[2] = {R0 + g < nb, R0 + 8 + g < nb};
+    const int sig = (g >> 1) + ((g & 1) ? 4 : 0);
+    const int spad = round_up(s, 8), scol = round_up(s, 16);
+    {
+      // columns s .. are zero (the solve's padded blocks multiply them by 0)
+      const int zcol = min(256, max(scol, round_up(n, 32) + 16));
+      const double* y0 = S.y + S.y_c_rb * rb;
+      for (int c0 = 0; c0 < zcol; c0 += 16) {
+        double v[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c0 + 4 * q + t;
+            v[q][h] = (okh[h] && c < s) ? __ldcs(y0 + (size_t)rowh[h] * s + c) : 0.0;
+          }
+        tm_st16(tl + 2 * c0, v);
+      }
+      tm_wait_st();
+    }
+    for (int p = 0; p < npanel; ++p) {
+      const int j0 = p * kP, nbp = min(kP, n - j0), kb = j0 & ~7;
+      mbar_wait(&s_ready[p], 0);
+      const double* tp = tglob + (size_t)p * kP * kP;
+      if (j0 + 2 * kP < n) {
+        block_reflector_apply<256>(A, lda, round_up(m, 8), j0, nbp, tp, true, j0 + 2 * kP, n, kP, 8);
+        ysync<256, 2>();
+        if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]);
+      }
+      tri_inverse32<256, 2>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, rglob + (size_t)npanel * kP * kP, 0);
+      // GEMM1: W = Y(:, kb:) V_p   (16 x 32)
+      double w[2][4][2] = {};
+      for (int kc = kb & ~15; kc < spad; kc += 16) {
+        double a[4][2];
+        tm_ld16(tl + 2 * kc, a);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = kc + 4 * u;
+          if (k < kb) continue;
+          if (k >= spad) break;
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const double bv = (k < j0 + kP) ? vval(A, lda, j0, nbp, k + t, 8 * f + g)
+                                            : ((8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0);
+            dmma8x8x4(w[0][f][0], w[0][f][1], a[u][0], bv);
+            dmma8x8x4(w[1][f][0], w[1][f][1], a[u][1], bv);
+          }
+        }
+      }
+      // GEMM2: W2 = W T_p
+      double w2[2][4][2] = {};
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        const double a0 = cfrag_to_afrag<4>(w[0], kk, lane);
+        const double a1 = cfrag_to_afrag<4>(w[1], kk, lane);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const double tb = __ldg(tp + (kk + t) * kP + 8 * f + g);
+          dmma8x8x4(w2[0][f][0], w2[0][f][1], a0, tb);
+          dmma8x8x4(w2[1][f][0], w2[1][f][1], a1, tb);
+        }
+      }
+      double a3[2][kP / 4];
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        a3[0][kk / 4] = -cfrag_to_afrag<4>(w2[0], kk, lane);
+        a3[1][kk / 4] = -cfrag_to_afrag<4>(w2[1], kk, lane);
+      }
+      // GEMM3: Y(:, kb:) -= W2 V_p^T, two 8-column blocks per TMEM access
+      for (int nc = kb & ~15; nc < spad; nc += 16) {
+        double cv[4][2];
+        tm_ld16(tl + 2 * nc, cv);
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          const int n0 = nc + 8 * hb;
+          if (n0 < kb || n0 >= spad) continue;
+          const int col = n0 + sig;
+#pragma unroll
+          for (int kk = 0; kk < kP; kk += 4) {
+            const double bv = (n0 < j0 + kP) ? vval(A, lda, j0, nbp, col, kk + t)
+                                             : ((kk + t < nbp) ? A[col + (j0 + kk + t) * lda] : 0.0);
+            dmma8x8x4(cv[2 * hb][0], cv[2 * hb + 1][0], a3[0][kk / 4], bv);
+            dmma8x8x4(cv[2 * hb][1], cv[2 * hb + 1][1], a3[1][kk / 4], bv);
+          }
+        }
+        tm_st16(tl + 2 * nc, cv);
+      }
+      tm_wait_st();
+      if (yw == 0 && lane == 0) FUSED_MARK(30 + p);
+    }
+    __threadfence_block();
+    ysync<256, 2>();   // every diagonal-block inverse of R is in rglob
+    if (yw == 0 && lane == 0) FUSED_MARK(40);
+    // blocked back substitution X R^T = Y Q1 on the TMEM rows (columns < n)
+    for (int blk = npanel - 1; blk >= 0; --blk) {
+      const int i0 = blk * kP, c0 = i0 + kP;
+      const int kr = n > c0 ? round_up(n - c0, 4) : 0;
+      double acc[2][4][2];
+      {
+        double v[4][2];
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {
+          tm_ld16(tl + 2 * (i0 + 16 * hq), v);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            acc[h][2 * hq][0] = v[0][h]; acc[h][2 * hq][1] = v[1][h];
+            acc[h][2 * hq + 1][0] = v[2][h]; acc[h][2 * hq + 1][1] = v[3][h];
+          }
+        }
+      }
+      for (int kc = 0; kc < kr; kc += 16) {
+        double av[4][2];
+        tm_ld16(tl + 2 * (c0 + kc), av);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = kc + 4 * u;
+          if (k >= kr) break;
+          const int c = c0 + k + t;
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const int i = i0 + 8 * f + sig;
+            const double bv = (i < n && c < n) ? A[i + c * lda] : 0.0;   // R(i, c)
+            dmma8x8x4(acc[0][f][0], acc[0][f][1], -av[u][0], bv);
+            dmma8x8x4(acc[1][f][0], acc[1][f][1], -av[u][1], bv);
+          }
+        }
+      }
+      const double* ri = rglob + (size_t)blk * kP * kP;
+      double xb[2][4][2] = {};
+#pragma unroll
+      for (int kk = 0; kk < kP; kk += 4) {
+        const double a0 = cfrag_to_afrag<4>(acc[0], kk, lane);
+        const double a1 = cfrag_to_afrag<4>(acc[1], kk, lane);
+        const int kq = (kk & 7) + t;
+        const int kact = 8 * (kk >> 3) + (kq >> 1) + ((kq & 1) ? 4 : 0);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const double bv = __ldcg(ri + (8 * f + sig) * kP + kact);   // R_blk^{-1}(j, k), permuted j and k
+          dmma8x8x4(xb[0][f][0], xb[0][f][1], a0, bv);
+          dmma8x8x4(xb[1][f][0], xb[1][f][1], a1, bv);
+        }
+      }
+      {
+        double v[4][2];
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int ff = 0; ff < 2; ++ff) {
+              const int f = 2 * hq + ff;
+              const int cA = i0 + 8 * f + t, cB = cA + 4;   // columns of positions 2t, 2t+1
+              v[2 * ff][h] = cA < n ? xb[h][f][0] : acc[h][f][0];
+              v[2 * ff + 1][h] = cB < n ? xb[h][f][1] : acc[h][f][1];
+            }
+          tm_st16(tl + 2 * (i0 + 16 * hq), v);
+        }
+      }
+      tm_wait_st();
+    }
+    // Y Q (X in columns < n, Y P in columns s-r .. s-1) back to the workspace
+    for (int c0 = 0; c0 < scol; c0 += 16) {
+      double v[4][2];
+      tm_ld16(tl + 2 * c0, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = c0 + 4 * q + t;
+          if (okh[h] && c < s) yq[(size_t)rowh[h] * s + c] = v[q][h];
+        }
+    }
+    tm_fence_before();
+    ysync<256, 2>();
+    tm_fence_after();
+    if (yw == 0) tm_dealloc512(tbase);
+    if (yw == 0 && lane == 0) FUSED_MARK(41);
+    return;
+  }
 #ifdef HBS_TRACE_NOY
   // timing experiment only: keep the far-trailing / ready hand-shakes, skip the Y work
   for (int p = 0; p < npanel; ++p) {
@@ -1837,21 +2034,36 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
 
 bool fused_fits(int s, int n_max) {
   const int lda = frag_ld(round_up(s, 32));
-  const size_t d = round_up(3 * n_max + kP + 34, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) + (size_t)lda * n_max;
+  const size_t d = round_up(3 * n_max + kP + 35, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) + (size_t)lda * n_max;
   return n_max <= 16 * kP && d * sizeof(double) <= kMaxSmemBytes;
+}
+
+template <int MR, bool TM>
+static int launch_fused_t(FusedArgs& args, int nsides, cudaStream_t stream) {
+  args.lda = frag_ld(round_up(args.s, 32));
+  const size_t d = round_up(3 * args.n_max + kP + 35, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
+                   (size_t)args.lda * args.n_max;
+  const size_t smem = d * sizeof(double);
+  cudaFuncSetAttribute(probe_fused_kernel<MR, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)args.geo.nbox, nsides);
+  probe_fused_kernel<MR, TM><<<grid, 512, smem, stream>>>(args);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+// Y rows in TMEM: at most 128 rows (lanes) and 256 fp64 columns per box
+static bool fused_tmem_ok(const FusedArgs& args) {
+#ifdef HBS_NO_TMEM
+  return false;
+#else
+  return args.n_max <= 128 && round_up(args.s, 16) <= 256;
+#endif
 }
 
 template <int MR>
 static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
-  args.lda = frag_ld(round_up(args.s, 32));
-  const size_t d = round_up(3 * args.n_max + kP + 34, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
-                   (size_t)args.lda * args.n_max;
-  const size_t smem = d * sizeof(double);
-  cudaFuncSetAttribute(probe_fused_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)args.geo.nbox, nsides);
-  probe_fused_kernel<MR><<<grid, 512, smem, stream>>>(args);
-  note_launch();
-  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+  return fused_tmem_ok(args) ? launch_fused_t<MR, true>(args, nsides, stream)
+                             : launch_fused_t<MR, false>(args, nsides, stream);
 }
 
 int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream) {
