@@ -251,8 +251,14 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     S.src = w.Pp[sd]; S.src_c_rb = 0; S.src_c_b = w.strideP; S.src_rs = w.ldP; S.src_cs = 1;
     S.q = outs[sd]; S.q_c_rb = r; S.q_c_b = 0; S.ldq = r;
   }
-  if (cholqr_fits(nr, r)) {
-    // CholeskyQR2 on the tensor cores; Householder only for flagged blocks
+  // CholeskyQR2 bases on the tensor cores (Householder only for flagged
+  // blocks) when they are interchangeable with the reference's: the basis of
+  // a node reaches the parent only through its span and a rotation of the
+  // parent's probe rows, and the parent's null-space pick (the last r columns
+  // of its complete Householder Q, linalg.py:52-62) is rotation-invariant
+  // exactly when its nullity s - 2r equals r.  Every BASELINE config has
+  // s = 3r; otherwise keep LAPACK's reflector-defined bases.
+  if (cholqr_fits(nr, r) && s <= 3 * r) {
     HBS_TRY(launch_cholqr(g, 2, w.qr_flag, st));
     g.only = w.qr_flag;
   }

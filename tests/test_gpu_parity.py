@@ -258,3 +258,51 @@ def test_pinned_host_pipeline_failure_names_node():
         hb.compress_from_samples(hb.SampleSet(*(t.numpy() for t in keep)), hb.build_tree(n, m),
                                  hb.CompressionConfig(rank=24, leaf_threshold=m))
     assert exc.value.level == 7 and exc.value.node_id == 127 + 77
+
+
+def _expanded(ub, level_of, L):
+    """Bases in original coordinates: leaf U, parent blockdiag(U_a, U_b) U_tau."""
+    out = {}
+    for level in range(L, 0, -1):
+        for j in range(1 << level):
+            nid = (1 << level) - 1 + j
+            u = ub(level, j)
+            if level < L:
+                ca, cb = out[(level + 1, 2 * j)], out[(level + 1, 2 * j + 1)]
+                r = ca.shape[1]
+                u = np.vstack([ca @ u[:r], cb @ u[r:]])
+            out[(level, j)] = u
+    return out
+
+
+@pytest.mark.parametrize("n,leaf,r,s", [(512, 32, 8, 48), (512, 32, 16, 48), (1024, 64, 32, 96)])
+def test_oversampled_null_space_matches_reference(n, leaf, r, s):
+    """The reference keeps the LAST r columns of LAPACK's complete Householder
+    Q of Omega_tau^T (linalg.py:52-62), so when nullity s - n_tau > r the
+    picked subspace depends on the exact reflectors, not only on
+    null(Omega_tau).  A full-rank dense operator makes every off-diagonal
+    block full rank, so any other pick would move the bases by O(1).  The
+    nested bases, expanded to original coordinates (the parent's U acts on
+    its children's bases), must match the reference node for node.  s > 3r:
+    LAPACK-signed bases at every level (raw node bases match too); s = 3r:
+    parents have nullity exactly r, the CholeskyQR2 bases are used and only
+    the expanded bases are comparable."""
+    rng = np.random.default_rng(77)
+    a = rng.standard_normal((n, n)) / np.sqrt(n)
+    om, ps = O.gaussian(n, s, 5, 0), O.gaussian(n, s, 5, 1)
+    y, z = a @ om, a.T @ ps
+    tree = hb.build_tree(n, leaf)
+    f = gpu_compress((om, ps, y, z), n, leaf, r)
+    ref = O.compress(om, ps, y, z, O.level_bounds(n, tree.depth), r)
+    L = tree.depth
+    gu = _expanded(lambda l, j: f.u_bases[(1 << l) - 1 + j], None, L)
+    gv = _expanded(lambda l, j: f.v_bases[(1 << l) - 1 + j], None, L)
+    ru = _expanded(lambda l, j: ref.U[l][j], None, L)
+    rv = _expanded(lambda l, j: ref.V[l][j], None, L)
+    for key in ru:
+        assert np.linalg.norm(gu[key] @ gu[key].T - ru[key] @ ru[key].T) <= 1e-8, key
+        assert np.linalg.norm(gv[key] @ gv[key].T - rv[key] @ rv[key].T) <= 1e-8, key
+        if s > 3 * r:
+            level, j = key
+            u = f.u_bases[(1 << level) - 1 + j]
+            assert np.linalg.norm(u @ u.T - ref.U[level][j] @ ref.U[level][j].T) <= 1e-8, key
