@@ -34,11 +34,10 @@ constexpr int kNmax = 128;          // max rows per box
 
 HBS_DEV void csync() { __syncthreads(); }
 
-// 1/sqrt(a) from the float estimate and two Newton steps in double (the
-// library routine's special-case handling dominates a Cholesky step); the
-// library covers operands outside the float range.
-HBS_DEV double rsqrt_fast(double a) {
-  if (!(a > 1e-30 && a < 1e30)) return rsqrt(a);
+// 1/sqrt(a) from the float estimate and two Newton steps in double, for
+// 1e-36 < a < 1e36 (callers check the range; the library routine's special-
+// case branches dominate a Cholesky step).
+HBS_DEV double rsqrt_nr(double a) {
   double y = static_cast<double>(rsqrtf(static_cast<float>(a)));
   const double ha = 0.5 * a;
   y = y * fma(-ha * y, y, 1.5);
@@ -46,10 +45,19 @@ HBS_DEV double rsqrt_fast(double a) {
   return y;
 }
 
+#ifdef HBS_TRACE
+__device__ long long g_cq_trace[32];
+#define CQ_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_cq_trace[i] = clock64(); } while (0)
+#else
+#define CQ_MARK(i) do { } while (0)
+#endif
+
 // G(0:rp, 0:rp) = A^T A for A (npad x rp, row-major, ld lda) on the tensor
 // cores; G column-major (G(i, j) at G[i + j*kLdG]); only blocks bi <= bj
 // (diagonal blocks in full).
-HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G) {
+// With e2 != nullptr also accumulates ||G - I||_F^2 over the leading r x r
+// part into *e2 (shared, zeroed by the caller) straight from the fragments.
+HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G, double* e2 = nullptr, int r = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int nbk = rp >> 3;
   const int nblk = nbk * (nbk + 1) / 2;
@@ -67,6 +75,17 @@ HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G) {
     const int i = 8 * bi + g, j = 8 * bj + 2 * t;
     G[i + j * kLdG] = c0 + d0;
     G[i + (j + 1) * kLdG] = c1 + d1;
+    if (e2) {
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = j + e;
+        const double v = (e ? c1 + d1 : c0 + d0) - (i == jj ? 1.0 : 0.0);
+        if (i <= jj && jj < r) acc = fma(i == jj ? v : 2.0 * v, v, acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) atomicAdd(e2, acc);
+    }
   }
 }
 
@@ -75,40 +94,39 @@ HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G) {
 // rdinv[o + j] = 1 / R(j, j).  One warp: lane k (and its mirror k + 16) owns
 // column o + k in registers; row j of R is broadcast through `row` (16
 // doubles, 16-byte aligned).  Returns false (warp-uniform) on breakdown.
-__device__ __noinline__ bool chol16(double* G, int o, const double* gdiag, double* rdinv, double* row) {
+HBS_DEV bool chol16(double* G, int o, const double* gdiag, double* rdinv, double* row) {
+  // branch-free body: every lane executes every shuffle and store (lanes
+  // 16..31 duplicate lanes 0..15 and write the same values), so the compiler
+  // needs no convergence barriers around the shuffles.
   const int lane = threadIdx.x & 31, kc = lane & 15;
   double c[16];
   double* col = G + o + (o + kc) * kLdG;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) c[i] = (i <= kc) ? col[i] : 0.0;
+  for (int i = 0; i < 16; ++i) c[i] = col[i];   // rows > kc are don't-care (masked below)
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const double d = __shfl_sync(0xffffffffu, c[j], j);
-    ok = ok && (d > 1e-12 * gdiag[o + j]) && (d < INFINITY);
-    const double rs = rsqrt_fast(d);
-    if (kc == j) c[j] = d * rs;
-    else if (kc > j) c[j] *= rs;
-    else c[j] = 0.0;
-    if (lane == j) rdinv[o + j] = rs;
-    if (lane < 16) row[lane] = c[j];
+    ok = ok && (d > 1e-12 * gdiag[o + j]) && (d > 1e-36) && (d < 1e36);
+    const double rs = rsqrt_nr(d);
+    c[j] = (kc == j) ? d * rs : (kc > j ? c[j] * rs : 0.0);
+    rdinv[o + j] = rs;
+    row[kc] = c[j];
     __syncwarp();
     const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
       if (2 * h + 1 > j) {
         const double2 v = r2[h];
-        if (2 * h > j && 2 * h <= kc) c[2 * h] = fma(-v.x, c[j], c[2 * h]);
-        if (2 * h + 1 <= kc) c[2 * h + 1] = fma(-v.y, c[j], c[2 * h + 1]);
+        if (2 * h > j) c[2 * h] = (2 * h <= kc) ? fma(-v.x, c[j], c[2 * h]) : c[2 * h];
+        c[2 * h + 1] = (2 * h + 1 <= kc) ? fma(-v.y, c[j], c[2 * h + 1]) : c[2 * h + 1];
       }
     }
     __syncwarp();
   }
-  if (lane < 16) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i <= kc) col[i] = c[i];
-  }
+  for (int i = 0; i < 16; ++i)
+    if (i <= kc && lane < 16) col[i] = c[i];
   return __all_sync(0xffffffffu, ok);
 }
 
@@ -153,7 +171,7 @@ HBS_DEV void schur_update(double* G, int o, int rc) {
 // the block's strictly lower triangle (Z(i, j), i < j, at
 // G[(o + j) + (o + i) * kLdG]); its diagonal is rdinv.  One warp; lane k
 // (k < 16) computes column k of Z by back substitution.
-__device__ __noinline__ void trinv16(double* G, int o, const double* rdinv) {
+HBS_DEV void trinv16(double* G, int o, const double* rdinv) {
   const int lane = threadIdx.x & 31, kc = lane & 15;
   double z[16];
 #pragma unroll
@@ -257,6 +275,41 @@ HBS_DEV void polar_b(double* G, int r, int rp, double* bdiag, bool second_order)
   }
 }
 
+// A <- A (I - F), F = upper triangle of E = G - I with the diagonal halved
+// (the Cholesky factor of I + E is I + F + O(||E||^2)); only the MMAs of the
+// upper block triangle are issued.
+HBS_DEV void apply_first_order(double* A, int lda, int npad, int r, int rp, const double* G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nbk = rp >> 3;
+  for (int rb = warp; rb < (npad >> 3); rb += kCT / 32) {
+    double* arow = A + (8 * rb) * lda;
+    double a[kRc / 4];
+#pragma unroll
+    for (int kk = 0; kk < kRc / 4; ++kk) a[kk] = (4 * kk < rp) ? arow[g * lda + 4 * kk + t] : 0.0;
+    double acc[kRc / 8][2];
+#pragma unroll
+    for (int f = 0; f < kRc / 8; ++f) { acc[f][0] = 0.0; acc[f][1] = 0.0; }
+#pragma unroll
+    for (int f = 0; f < kRc / 8; ++f) {
+      if (f >= nbk) break;
+#pragma unroll
+      for (int kk = 0; kk < 2 * f + 2; ++kk) {   // k <= 8 f + 7: the blocks on / above the diagonal
+        const int k = 4 * kk + t, c = 8 * f + g;
+        const double gv = G[k + c * kLdG];
+        const double fv = (k >= r || c >= r) ? 0.0 : (k < c ? gv : (k == c ? 0.5 * (gv - 1.0) : 0.0));
+        dmma8x8x4(acc[f][0], acc[f][1], a[kk], fv);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < kRc / 8; ++f) {
+      if (f >= nbk) break;
+      arow[g * lda + 8 * f + 2 * t] -= acc[f][0];
+      arow[g * lda + 8 * f + 2 * t + 1] -= acc[f][1];
+    }
+  }
+}
+
 // A <- A B for the symmetric B of polar_b.
 HBS_DEV void apply_b(double* A, int lda, int npad, int rp, const double* G, const double* bdiag) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -294,13 +347,14 @@ HBS_DEV void apply_b(double* A, int lda, int npad, int rp, const double* G, cons
 // Returns false on breakdown.
 HBS_DEV bool cholesky_pass(double* A, int lda, int npad, int rc, double* G, const double* gdiag, double* rdinv,
                            int* s_ok, double* rowbuf) {
-  const int warp = threadIdx.x >> 5;
+  const int warp = uniform_warp(threadIdx.x >> 5);   // provably warp-uniform branches
   for (int o = 0; o < rc; o += 16) {
     if (warp == 0) {
       const bool ok = chol16(G, o, gdiag, rdinv, rowbuf);
       if (threadIdx.x == 0) *s_ok = ok;
     }
     csync();
+    CQ_MARK(8 + o / 16);
     if (!*s_ok) return false;
     if (o + 16 < rc) {
       trsm_row(G, o, rc, rdinv);
@@ -309,10 +363,13 @@ HBS_DEV bool cholesky_pass(double* A, int lda, int npad, int rc, double* G, cons
       csync();
     }
   }
+  CQ_MARK(12);
   if (warp < (rc >> 4)) trinv16(G, 16 * warp, rdinv);
   csync();
+  CQ_MARK(13);
   apply_rinv(A, lda, npad, rc, G, rdinv);
   csync();
+  CQ_MARK(14);
   return true;
 }
 
@@ -331,11 +388,12 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
   double* rdinv = gdiag + kRc;            // kRc
   double* rowbuf = rdinv + kRc;           // 32 (Cholesky row broadcast)
   int* s_ok = reinterpret_cast<int*>(rowbuf + 32);
-  double* s_e2 = rowbuf + 33;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(rowbuf + 34);
-  double* A = rowbuf + 36;                // npad x lda (16-byte aligned rows)
+  double* s_e2 = rowbuf + 36;             // per pass ||G - I||_F^2
+  double* A = rowbuf + 40;                // npad x lda (16-byte aligned rows)
   int32_t* myflag = flag + (int64_t)side * args.geo.nbox + b;
 
+  CQ_MARK(0);
   const int64_t rb = args.geo.row_begin[b];
   const double* src = S.src + S.src_c_rb * rb + S.src_c_b * b;
   // rows are contiguous r-double runs: one TMA bulk copy per row when aligned
@@ -361,13 +419,16 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
     }
   }
   for (int e = threadIdx.x; e < kRc * kLdG; e += kCT) G[e] = 0.0;
+  if (threadIdx.x < 3) s_e2[threadIdx.x] = 0.0;
   if (bulk) mbar_wait(s_bar, 0);
   csync();
+  CQ_MARK(1);
 
   bool fail = nb < r;
   for (int pass = 0; pass < 3 && !fail; ++pass) {
-    gram(A, lda, npad, rp, G);
+    gram(A, lda, npad, rp, G, pass ? s_e2 + pass : nullptr, r);
     csync();
+    CQ_MARK(2 + 3 * pass);
     if (pass == 0) {
       for (int j = threadIdx.x; j < rc; j += kCT) {
         if (j >= r) {   // identity padding of the Cholesky dimension
@@ -377,25 +438,22 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
       }
       csync();
     } else {
-      // ||E||_F^2, E = G - I: polar finish A (I + E)^{-1/2} when ||E||_F <= 1e-5
-      double e2 = 0.0;
-      for (int q = threadIdx.x; q < r * r; q += kCT) {
-        const int i = q % r, j = q / r;
-        if (i <= j) {
-          const double v = G[i + j * kLdG] - (i == j ? 1.0 : 0.0);
-          e2 = fma(i == j ? v : 2.0 * v, v, e2);
-        }
-      }
-      e2 = warp_sum(e2);
-      if (threadIdx.x == 0) *s_e2 = 0.0;
-      csync();
-      if ((threadIdx.x & 31) == 0) atomicAdd(s_e2, e2);
-      csync();
-      if (*s_e2 <= 1e-10) {
-        polar_b(G, r, rp, rdinv, *s_e2 > 1e-16);
+      // ||E||_F^2 (E = G - I, accumulated by gram): first-order Cholesky
+      // finish when ||E||_F <= 1e-8, polar finish when <= 1e-5
+      const double e2 = s_e2[pass];
+      if (e2 <= 1e-16) {
+        apply_first_order(A, lda, npad, r, rp, G);
         csync();
+        CQ_MARK(16);
+        break;
+      }
+      if (e2 <= 1e-10) {
+        polar_b(G, r, rp, rdinv, true);
+        csync();
+        CQ_MARK(15);
         apply_b(A, lda, npad, rp, G, rdinv);
         csync();
+        CQ_MARK(16);
         break;
       }
       if (pass == 2) { fail = true; break; }
@@ -422,7 +480,16 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
 bool cholqr_fits(int n_max, int r) { return n_max <= kNmax && r <= kRc && r >= 1; }
 
 size_t cholqr_smem_bytes(int n_max, int r) {
-  return ((size_t)kRc * kLdG + 2 * kRc + 36 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
+  return ((size_t)kRc * kLdG + 2 * kRc + 40 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
+}
+
+extern "C" int hbs_debug_cq_trace(long long* out) {
+#ifdef HBS_TRACE
+  return cudaMemcpyFromSymbol(out, g_cq_trace, sizeof(long long) * 32) == cudaSuccess ? 0 : 4;
+#else
+  (void)out;
+  return 6;
+#endif
 }
 
 int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream) {
