@@ -55,12 +55,14 @@ __device__ long long g_cq_trace[32];
 // G(0:rp, 0:rp) = A^T A for A (npad x rp, row-major, ld lda) on the tensor
 // cores; G column-major (G(i, j) at G[i + j*kLdG]); only blocks bi <= bj
 // (diagonal blocks in full).
-// With e2 != nullptr also accumulates ||G - I||_F^2 over the leading r x r
-// part into *e2 (shared, zeroed by the caller) straight from the fragments.
-HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G, double* e2 = nullptr, int r = 0) {
+// With e2w != nullptr also forms ||G - I||_F^2 over the leading r x r part
+// straight from the fragments: warp w stores its partial sum in e2w[w]
+// (deterministic: the caller adds the eight partials in a fixed order).
+HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G, double* e2w = nullptr, int r = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int nbk = rp >> 3;
   const int nblk = nbk * (nbk + 1) / 2;
+  double e2acc = 0.0;
   for (int q = warp; q < nblk; q += kCT / 32) {
     int bi = 0, rem = q;
     while (rem >= nbk - bi) { rem -= nbk - bi; ++bi; }
@@ -75,17 +77,18 @@ HBS_DEV void gram(const double* A, int lda, int npad, int rp, double* G, double*
     const int i = 8 * bi + g, j = 8 * bj + 2 * t;
     G[i + j * kLdG] = c0 + d0;
     G[i + (j + 1) * kLdG] = c1 + d1;
-    if (e2) {
-      double acc = 0.0;
+    if (e2w) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int jj = j + e;
         const double v = (e ? c1 + d1 : c0 + d0) - (i == jj ? 1.0 : 0.0);
-        if (i <= jj && jj < r) acc = fma(i == jj ? v : 2.0 * v, v, acc);
+        if (i <= jj && jj < r) e2acc = fma(i == jj ? v : 2.0 * v, v, e2acc);
       }
-      acc = warp_sum(acc);
-      if (lane == 0) atomicAdd(e2, acc);
     }
+  }
+  if (e2w) {
+    e2acc = warp_sum(e2acc);
+    if (lane == 0) e2w[warp] = e2acc;
   }
 }
 
@@ -389,8 +392,8 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
   double* rowbuf = rdinv + kRc;           // 32 (Cholesky row broadcast)
   int* s_ok = reinterpret_cast<int*>(rowbuf + 32);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(rowbuf + 34);
-  double* s_e2 = rowbuf + 36;             // per pass ||G - I||_F^2
-  double* A = rowbuf + 40;                // npad x lda (16-byte aligned rows)
+  double* s_e2 = rowbuf + 36;             // per-warp partials of ||G - I||_F^2
+  double* A = rowbuf + 44;                // npad x lda (16-byte aligned rows)
   int32_t* myflag = flag + (int64_t)side * args.geo.nbox + b;
 
   CQ_MARK(0);
@@ -419,14 +422,13 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
     }
   }
   for (int e = threadIdx.x; e < kRc * kLdG; e += kCT) G[e] = 0.0;
-  if (threadIdx.x < 3) s_e2[threadIdx.x] = 0.0;
   if (bulk) mbar_wait(s_bar, 0);
   csync();
   CQ_MARK(1);
 
   bool fail = nb < r;
   for (int pass = 0; pass < 3 && !fail; ++pass) {
-    gram(A, lda, npad, rp, G, pass ? s_e2 + pass : nullptr, r);
+    gram(A, lda, npad, rp, G, pass ? s_e2 : nullptr, r);
     csync();
     CQ_MARK(2 + 3 * pass);
     if (pass == 0) {
@@ -440,7 +442,9 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
     } else {
       // ||E||_F^2 (E = G - I, accumulated by gram): first-order Cholesky
       // finish when ||E||_F <= 1e-8, polar finish when <= 1e-5
-      const double e2 = s_e2[pass];
+      double e2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kCT / 32; ++w) e2 += s_e2[w];
       if (e2 <= 1e-16) {
         apply_first_order(A, lda, npad, r, rp, G);
         csync();
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t*
 bool cholqr_fits(int n_max, int r) { return n_max <= kNmax && r <= kRc && r >= 1; }
 
 size_t cholqr_smem_bytes(int n_max, int r) {
-  return ((size_t)kRc * kLdG + 2 * kRc + 40 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
+  return ((size_t)kRc * kLdG + 2 * kRc + 44 + (size_t)round_up(n_max, 8) * frag_ld(round_up(r, 16))) * sizeof(double);
 }
 
 extern "C" int hbs_debug_cq_trace(long long* out) {
