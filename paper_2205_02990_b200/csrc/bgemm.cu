@@ -7,8 +7,10 @@
 // telescoping apply used by the HBS sampler (factorization.py:89-143).
 //
 // 64 x 64 CTA tile, 4 warps of 32 x 32 (16 MMAs per 8 fragment loads per
-// k-step), BK = 16, 3-stage cp.async pipeline (3 CTAs per SM) with 16-byte
-// copies when every operand row start of the box is 16-byte aligned.  Each operand is staged in the
+// k-step), BK = 16, double-buffered cp.async with 16-byte copies when every
+// operand row start of the box is 16-byte aligned; 96 registers and 41 KB of
+// shared memory give 5 CTAs per SM (measured best for the K = 64..192
+// per-box products: more resident warps beat deeper pipelines).  Each operand is staged in the
 // orientation it has in global memory (contiguous runs stay contiguous), and
 // both staging layouts give bank-conflict-free m8n8k4 fragment loads.
 #include "common.cuh"
@@ -17,7 +19,16 @@
 namespace hbs {
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3, NT = 128;
+#ifndef BGEMM_BK
+#define BGEMM_BK 16
+#endif
+#ifndef BGEMM_NSTAGE
+#define BGEMM_NSTAGE 2
+#endif
+#ifndef BGEMM_MINB
+#define BGEMM_MINB 5   // 5 CTAs (20 warps) per SM: these short-K products are latency-bound
+#endif
+constexpr int BM = 64, BN = 64, BK = BGEMM_BK, NSTAGE = BGEMM_NSTAGE, NT = 128;
 constexpr int LDK = BK + 4;   // k-contiguous staging: [row][k]  (== 4 mod 16)
 constexpr int LDR = BM + 4;   // row-contiguous staging: [k][row]
 constexpr int STAGE = BM * LDK > BK * LDR ? BM * LDK : BK * LDR;   // doubles per operand stage
@@ -44,7 +55,7 @@ HBS_DEV void stage_tile(double* s, const double* p, int ld, int i0, int k0, int 
     for (int e = 0; e < (BM * BK / 2) / NT; ++e) {
       const int idx = tid + e * NT;
       int i, k;
-      if (KC) { i = idx >> 3; k = 2 * (idx & 7); }
+      if (KC) { i = idx / (BK / 2); k = 2 * (idx % (BK / 2)); }
       else { k = idx >> 5; i = 2 * (idx & 31); }
       const int gi = i0 + i, gk = k0 + k;
       int bytes;
@@ -63,7 +74,7 @@ HBS_DEV void stage_tile(double* s, const double* p, int ld, int i0, int k0, int 
     for (int e = 0; e < (BM * BK) / NT; ++e) {
       const int idx = tid + e * NT;
       int i, k;
-      if (KC) { i = idx >> 4; k = idx & 15; }
+      if (KC) { i = idx / BK; k = idx % BK; }
       else { k = idx >> 6; i = idx & 63; }
       const int gi = i0 + i, gk = k0 + k;
       const bool ok = gi < I && gk < K;
@@ -85,7 +96,7 @@ HBS_DEV double frag(const double* s, int row, int k) {
 HBS_DEV bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <bool AKC, bool BKC>
-__global__ void __launch_bounds__(NT, 3) bgemm_kernel(BgemmArgs args) {
+__global__ void __launch_bounds__(NT, BGEMM_MINB) bgemm_kernel(BgemmArgs args) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                       // NSTAGE x STAGE
   double* Bs = smem + NSTAGE * STAGE;      // NSTAGE x STAGE
