@@ -13,6 +13,7 @@ its node id and level (compress.py:260-265, 274-279).
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -131,7 +132,7 @@ class CompressPlan:
     the lifted quadruple of the last compressed level (the multi-GPU hand-off)."""
 
     def __init__(self, tree: ClusterTree, s: int, rank: int, tol: float = DEFAULT_ILL_CONDITIONING_TOL,
-                 device=None, specs=None, with_root=None):
+                 device=None, specs=None, with_root=None, out_levels=None):
         self.tree, self.s, self.rank, self.tol = tree, s, rank, tol
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         r = rank
@@ -145,9 +146,12 @@ class CompressPlan:
         for level, begins, first in self.specs:
             g = LevelGeometry(begins, dev)
             self.geometry[level], self.first_box[level] = g, first
-            self.levels[level] = (torch.empty(g.total_rows, r, dtype=f64, device=dev),
-                                  torch.empty(g.total_rows, r, dtype=f64, device=dev),
-                                  torch.empty(g.sq_total, dtype=f64, device=dev))
+            if out_levels is not None and level in out_levels:   # caller-owned (views of full levels)
+                self.levels[level] = out_levels[level]
+            else:
+                self.levels[level] = (torch.empty(g.total_rows, r, dtype=f64, device=dev),
+                                      torch.empty(g.total_rows, r, dtype=f64, device=dev),
+                                      torch.empty(g.sq_total, dtype=f64, device=dev))
             sz = _size_t()
             _native.check(lib.hbs_level_workspace_bytes(g.nbox, g.max_rows, s, r, ctypes.byref(sz)), "workspace")
             ws = max(ws, sz.value)
@@ -328,85 +332,104 @@ def _pinned_view(a):
     return t if t.is_pinned() else None
 
 
-def _compress_host_pipelined(host, tree: ClusterTree, config: CompressionConfig, dev, chunks: int = 8):
+def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, dev, chunks: int = None):
     """Host (pinned) samples in, host-materialised factorization out, with the
-    transfers overlapped: the leaf level streams in `chunks` runs of boxes
-    (H2D of run c+1 on a copy stream while run c computes), and every level's
-    U, V, D go back to pinned host memory on the copy stream as soon as they
-    are final, while the coarser levels compute."""
+    transfers hidden behind the compute by subtree: the rows are uploaded as
+    `chunks` contiguous subtrees (one H2D stream), each subtree is compressed
+    from its leaves up to its own root as soon as its rows have arrived (the
+    single-device form of the multi-GPU partition, distributed.py), its
+    U, V, D go back to pinned host memory on a second copy stream while the
+    next subtree computes, and the few top levels plus the root run on the
+    concatenated subtree-root lifts at the end.  Per-node arithmetic is that
+    of the level sweep, so the result is bitwise identical to it
+    (test_host_subtree_pipeline_bitwise)."""
+    from .distributed import SubtreePartition
     from .factorization import LevelGeometry
     n, s = host[0].shape
     r, tol = config.rank, config.ill_conditioning_tol
-    plan = CompressPlan(tree, s, r, tol, dev)
-    comp = torch.cuda.current_stream(dev)
-    h2d = torch.cuda.Stream(dev)      # separate copy streams: PCIe is full duplex
-    copy = torch.cuda.Stream(dev)     # device -> host
     L = tree.depth
-    g = plan.geometry[L]
-    nb = g.nbox
-    chunks = max(1, min(chunks, nb))
-    edges = [round(i * nb / chunks) for i in range(chunks + 1)]
-    dq = [torch.empty(n, s, dtype=torch.float64, device=dev) for _ in range(4)]
-    # per-level pinned destinations
-    hosts = {}
-    for lv, (u, v, d) in plan.levels.items():
-        hosts[lv] = tuple(torch.empty(t.shape, dtype=torch.float64, pin_memory=True) for t in (u, v, d))
-    statuses, evs, arrived = [], [], []
-    for c in range(chunks):       # all uploads first, back to back on the H2D stream
-        b0, b1 = edges[c], edges[c + 1]
-        r0, r1 = int(g.begins_host[b0]), int(g.begins_host[b1])
+    if chunks is None:
+        chunks = int(os.environ.get("HBS_HOST_CHUNKS", "8"))
+    world = 1
+    while world * 2 <= chunks and (world * 2).bit_length() - 1 < L:
+        world *= 2
+    full = {lv: b for lv, b, _ in tree_level_specs(tree, r)}
+    geo = {lv: LevelGeometry(full[lv], dev) for lv in full}
+    f64 = torch.float64
+    levels = {lv: (torch.empty(g.total_rows, r, dtype=f64, device=dev), torch.empty(g.total_rows, r, dtype=f64, device=dev),
+                   torch.empty(g.sq_total, dtype=f64, device=dev)) for lv, g in geo.items()}
+    hosts = {lv: tuple(torch.empty(t.shape, dtype=f64, pin_memory=True) for t in ts) for lv, ts in levels.items()}
+    comp = torch.cuda.current_stream(dev)
+    h2d, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    dq = [torch.empty(n, s, dtype=f64, device=dev) for _ in range(4)]
+    parts = [SubtreePartition(tree, world, g, r) for g in range(world)]
+    def views(specs):
+        out = {}
+        for lv, begins, first in specs:
+            g, nb = geo[lv], len(begins) - 1
+            r0, r1 = int(g.begins_host[first]), int(g.begins_host[first + nb])
+            q0, q1 = int(g.sq_host[first]), int(g.sq_host[first + nb])
+            out[lv] = (r0, r1, q0, q1)
+        return out
+
+    def drain(specs, plan):       # level blocks of `plan` -> pinned host, on the copy stream
+        done = torch.cuda.Event()
+        done.record(comp)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            for lv, (r0, r1, q0, q1) in views(specs).items():
+                u, v, d = levels[lv]
+                hu, hv, hd = hosts[lv]
+                hu[r0:r1].copy_(u[r0:r1], non_blocking=True)
+                hv[r0:r1].copy_(v[r0:r1], non_blocking=True)
+                hd[q0:q1].copy_(d[q0:q1], non_blocking=True)
+
+    def out_views(specs):
+        return {lv: (levels[lv][0][r0:r1], levels[lv][1][r0:r1], levels[lv][2][q0:q1])
+                for lv, (r0, r1, q0, q1) in views(specs).items()}
+
+    # every plan (buffers, geometry uploads) is built before any compute is
+    # enqueued, so the launches of consecutive subtrees go out back to back
+    plans = [CompressPlan(tree, s, r, tol, dev, specs=p.local_specs, with_root=(world == 1),
+                          out_levels=out_views(p.local_specs)) for p in parts]
+    tspecs = parts[0].top_specs
+    top = plans[0] if world == 1 else CompressPlan(tree, s, r, tol, dev, specs=tspecs, with_root=True,
+                                                   out_levels=out_views(tspecs))
+    # (uploads after the plans: their small geometry copies must not queue
+    # behind gigabytes of H2D on the copy engine)
+    arrived = []
+    for p in parts:              # all uploads back to back on the H2D stream
         with torch.cuda.stream(h2d):
             for i in range(4):
-                dq[i][r0:r1].copy_(host[i][r0:r1], non_blocking=True)
+                dq[i][p.begin:p.end].copy_(host[i][p.begin:p.end], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(h2d)
         arrived.append(ev)
-    geos = [LevelGeometry(g.begins_host[edges[c]:edges[c + 1] + 1], dev) for c in range(chunks)]
-    for c in range(chunks):
-        b0, b1 = edges[c], edges[c + 1]
-        r0, r1 = int(g.begins_host[b0]), int(g.begins_host[b1])
-        ev, geo = arrived[c], geos[c]
-        stat = torch.zeros(2 * (b1 - b0), dtype=torch.int32, device=dev)
+
+    for p, ev, plan in zip(parts, arrived, plans):
         comp.wait_event(ev)
-        plan.run_level(0, dq, comp.cuda_stream, box_range=(b0, b1), chunk_geo=geo, status=stat)
-        done = torch.cuda.Event()
-        done.record(comp)
-        copy.wait_event(done)
-        u, v, d = plan.levels[L]
-        hu, hv, hd = hosts[L]
-        sq0, sq1 = int(g.sq_host[b0]), int(g.sq_host[b1])
-        with torch.cuda.stream(copy):
-            hu[r0:r1].copy_(u[r0:r1], non_blocking=True)
-            hv[r0:r1].copy_(v[r0:r1], non_blocking=True)
-            hd[sq0:sq1].copy_(d[sq0:sq1], non_blocking=True)
-        statuses.append((b0, stat))
-        evs.append((geo, ev, done))
-    quad = tuple(m[:nb * r] for m in plan.lift[0])
-    for idx in range(1, len(plan.specs)):
-        quad = plan.run_level(idx, quad, comp.cuda_stream)
-        lv = plan.specs[idx][0]
-        done = torch.cuda.Event()
-        done.record(comp)
-        copy.wait_event(done)
-        with torch.cuda.stream(copy):
-            for t, h in zip(plan.levels[lv], hosts[lv]):
-                h.copy_(t, non_blocking=True)
-    plan.top_quad = quad
-    plan.run_root(quad[0], quad[2], stream=comp.cuda_stream)
+        plan.run(*[m[p.begin:p.end] for m in dq], stream=comp.cuda_stream)
+        drain(p.local_specs, plan)
+    if world > 1:
+        with torch.cuda.stream(comp):
+            top_quad = tuple(torch.cat([pl.top_quad[i] for pl in plans]) for i in range(4))
+        if tspecs:
+            top.run(*top_quad, stream=comp.cuda_stream)
+            drain(tspecs, top)
+        else:
+            top.run_root(top_quad[0], top_quad[2], stream=comp.cuda_stream)
+        plans = plans + [top]
     torch.cuda.synchronize(dev)
-    # failures in sweep order: leaf chunks first (ascending boxes), then the rest
-    for b0, stat in statuses:
-        hs = stat.cpu().numpy()
-        k = hs.size // 2
-        bad = np.nonzero(hs.reshape(2, k).any(axis=0))[0]
-        if bad.size:
-            raise_ill_conditioned(L, (1 << L) - 1 + b0 + int(bad[0]), tol)
-    plan.raise_for_status_from(1)
-    f = plan.factorization()
+    fails = [f for f in (pl.first_failure() for pl in plans) if f is not None]
+    if fails:
+        level, nid = min(fails, key=lambda f: (-f[0], f[1]))
+        raise_ill_conditioned(level, nid, tol)
+    geo_list = [geo.get(lv, top.geometry[0] if lv == 0 else None) for lv in range(L + 1)]
+    f = HbsFactorization.from_device(tree, r, geo_list, [None] + [levels[lv] for lv in range(1, L + 1)], top.root)
     for lv, (hu, hv, hd) in hosts.items():
         f._host[(lv, "u")], f._host[(lv, "v")], f._host[(lv, "d")] = hu.numpy(), hv.numpy(), hd.numpy()
-    f._host["root"] = plan.root.cpu().numpy()
-    f._host_keepalive = (hosts, dq)
+    f._host["root"] = top.root.cpu().numpy()
+    f._host_keepalive = (hosts, dq, plans)
     return f
 
 
@@ -427,7 +450,7 @@ def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: Compres
         raise DimensionError("the compressor runs on a CUDA device only (no CPU fallback)")
     pinned = [_pinned_view(m) for m in (samples.omega, samples.psi, samples.y, samples.z)]
     if all(p is not None for p in pinned) and tree.depth >= 2:
-        f = _compress_host_pipelined(pinned, tree, config, dev)
+        f = _compress_host_subtrees(pinned, tree, config, dev)
         if flops.counting():
             _charge_madds(tree, s, r)
         return f

@@ -231,7 +231,7 @@ def _pinned(a):
 
 @pytest.mark.parametrize("name", ["c1_twin", "uneven_333", "c4_shape_literal"])
 def test_pinned_host_pipeline_bitwise(name):
-    """Pinned host samples take the overlapped path (chunked leaf uploads,
+    """Pinned host samples take the overlapped path (subtree-chunked uploads,
     per-level downloads on a second stream); results equal the plain path
     bit for bit, and the dict views come back already on the host."""
     c = golden_cases.load(name)
