@@ -67,6 +67,16 @@ def canonical_total_flops(tree, s, r):
     return total
 
 
+def fused_traffic():
+    """DRAM bytes per launch of the dominant (fused) kernel from the committed
+    ncu --set full capture (profiles/fused_traffic_r01.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fused_traffic_r01.json")) as fh:
+            return float(json.load(fh)["traffic_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def fp64_peak():
     path = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
     with open(path) as fh:
@@ -388,7 +398,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox generator, seeded)",
             "config": config_block(args, cfg, world),
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak_tf, "traffic": fused_traffic(), "peak_source": peak_src,
                          "step_achieved": step_tf, "step_frac": step_tf / peak_tf,
                          "step_canonical_flops": total_flops,
                          "phase_ms": phase_ms, "phase_tflops": {p: (phase_flops[p] / (phase_ms[p] / 1e3) / 1e12
