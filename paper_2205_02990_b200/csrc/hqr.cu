@@ -1545,7 +1545,17 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         FUSED_MARK(20);
       }
     }
-    if constexpr (TM) return;   // the solve runs on the TMEM-resident rows (group Y)
+    if constexpr (TM) {
+      // the solve runs on the TMEM-resident rows (group Y); group P, idle
+      // from here on, inverts R's last diagonal block for it while group Y
+      // applies the last panel (scratch: Tscr, free after the last form_t)
+      const int jl = (npanel - 1) * kP;
+      tri_inverse32<256, 1>(A, lda, jl, min(kP, n - jl), rglob + (size_t)(npanel - 1) * kP * kP, Tscr, 8);
+      __threadfence_block();
+      gsync<256>();
+      if (lt == 0) mbar_arrive(&s_ready[32]);
+      return;
+    }
     // group Y has applied every panel and inverted every diagonal block of R:
     // take row groups lt/32 (mod 16) of the solve
     mbar_wait(&s_ready[32], 0);
@@ -1593,7 +1603,8 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         ysync<256, 2>();
         if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]);
       }
-      tri_inverse32<256, 2>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, rglob + (size_t)npanel * kP * kP, 0);
+      if (p + 1 < npanel)   // (the last block is inverted by group P)
+        tri_inverse32<256, 2>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, rglob + (size_t)npanel * kP * kP, 0);
       // GEMM1: W = Y(:, kb:) V_p   (16 x 32)
       double w[2][4][2] = {};
       for (int kc = kb & ~15; kc < spad; kc += 16) {
@@ -1655,7 +1666,8 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       if (yw == 0 && lane == 0) FUSED_MARK(30 + p);
     }
     __threadfence_block();
-    ysync<256, 2>();   // every diagonal-block inverse of R is in rglob
+    ysync<256, 2>();   // every diagonal-block inverse of R is in rglob ...
+    mbar_wait(&s_ready[32], 0);   // ... including the last one (group P)
     if (yw == 0 && lane == 0) FUSED_MARK(40);
     // blocked back substitution X R^T = Y Q1 on the TMEM rows (columns < n)
     for (int blk = npanel - 1; blk >= 0; --blk) {
