@@ -1792,119 +1792,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     }
     // R's diagonal block p is final: its inverse for the solve
     tri_inverse32<256, 2>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, rglob + (size_t)npanel * kP * kP, 0);
-#ifdef HBS_YPAIR
-    // two 8-row groups (rg, rg + 8) per warp pass: every V_p fragment read
-    // from shared memory feeds two MMAs, and both groups' loads are in flight
-    for (int rg = yw; rg < ngroups; rg += 16) {
-      const bool two = rg + 8 < ngroups;   // warp-uniform
-      const double* srowh[2];
-      double* drowh[2];
-      bool rokh[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = 8 * (rg + 8 * h) + g;
-        rokh[h] = row < nb;
-        srowh[h] = (p == 0 ? y0 : yq) + (size_t)(rokh[h] ? row : 0) * s;
-        drowh[h] = yq + (size_t)(rokh[h] ? row : 0) * s;
-      }
-      // GEMM1: W = Y(:, kb:) V_p   (16 x 32)
-      double w[2][4][2] = {};
-      for (int kc = kb; kc < spad; kc += 32) {
-        double av[2][8];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int col = kc + 4 * u + t;
-            av[h][u] = (rokh[h] && col < s && kc + 4 * u < spad) ? __ldcg(srowh[h] + col) : 0.0;
-          }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int k = kc + 4 * u;
-          if (k >= spad) break;
-          if (k < j0 + kP) {
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const double bv = vval(A, lda, j0, nbp, k + t, 8 * f + g);
-              dmma8x8x4(w[0][f][0], w[0][f][1], av[0][u], bv);
-              if (two) dmma8x8x4(w[1][f][0], w[1][f][1], av[1][u], bv);
-            }
-          } else {
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const double bv = (8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0;
-              dmma8x8x4(w[0][f][0], w[0][f][1], av[0][u], bv);
-              if (two) dmma8x8x4(w[1][f][0], w[1][f][1], av[1][u], bv);
-            }
-          }
-        }
-      }
-      // GEMM2: W2 = W T_p, T fragments from L1
-      double w2[2][4][2] = {};
-#pragma unroll
-      for (int kk = 0; kk < kP; kk += 4) {
-        const double a0 = cfrag_to_afrag<4>(w[0], kk, lane);
-        const double a1 = cfrag_to_afrag<4>(w[1], kk, lane);
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const double tb = __ldg(tp + (kk + t) * kP + 8 * f + g);
-          dmma8x8x4(w2[0][f][0], w2[0][f][1], a0, tb);
-          if (two) dmma8x8x4(w2[1][f][0], w2[1][f][1], a1, tb);
-        }
-      }
-      double a3[2][kP / 4];
-#pragma unroll
-      for (int kk = 0; kk < kP; kk += 4) {
-        a3[0][kk / 4] = -cfrag_to_afrag<4>(w2[0], kk, lane);
-        a3[1][kk / 4] = -cfrag_to_afrag<4>(w2[1], kk, lane);
-      }
-      // GEMM3: Y(:, kb:) -= W2 V_p^T  (first panel also copies columns < kb)
-      if (p == 0) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          for (int c = 2 * t; c < kb; c += 8)
-            if (rokh[h]) st2(drowh[h] + c, ld2(srowh[h] + c, c + 1 < kb), c + 1 < kb);
-      }
-      for (int nc = kb; nc < spad; nc += 16) {
-        double2 cv[2][2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int col = nc + 8 * u + 2 * t;
-            cv[h][u] = (rokh[h] && col < s) ? ld2(srowh[h] + col, col + 1 < s) : make_double2(0.0, 0.0);
-          }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int n0 = nc + 8 * u;
-          if (n0 >= spad) break;
-          if (n0 < j0 + kP) {
-#pragma unroll
-            for (int kk = 0; kk < kP; kk += 4) {
-              const double bv = vval(A, lda, j0, nbp, n0 + g, kk + t);
-              dmma8x8x4(cv[0][u].x, cv[0][u].y, a3[0][kk / 4], bv);
-              if (two) dmma8x8x4(cv[1][u].x, cv[1][u].y, a3[1][kk / 4], bv);
-            }
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < kP; kk += 4) {
-              const double bv = (kk + t < nbp) ? A[(n0 + g) + (j0 + kk + t) * lda] : 0.0;
-              dmma8x8x4(cv[0][u].x, cv[0][u].y, a3[0][kk / 4], bv);
-              if (two) dmma8x8x4(cv[1][u].x, cv[1][u].y, a3[1][kk / 4], bv);
-            }
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int col = nc + 8 * u + 2 * t;
-            if (rokh[h] && col < s && nc + 8 * u < spad) st2(drowh[h] + col, cv[h][u], col + 1 < s);
-          }
-      }
-      __syncwarp();
-    }
-#else
     for (int rg = yw; rg < ngroups; rg += 8) {
       const int row = 8 * rg + g;
       const bool rok = row < nb;
@@ -1912,33 +1799,13 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       double* drow = yq + (size_t)row * s;
       // GEMM1: W = Y(:, kb:) V_p   (8 x 32); A-fragment loads issued 32 columns ahead
       double w[4][2] = {};
-#ifdef HBS_YPF
-      double av[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int col = kb + 4 * u + t;
-        av[u] = (rok && col < s && kb + 4 * u < spad) ? __ldcg(srow + col) : 0.0;
-      }
-#endif
       for (int kc = kb; kc < spad; kc += 32) {
-#ifdef HBS_YPF
-        // next chunk's A-fragments in flight while this chunk's MMAs issue
-        double an[8];
-        if (kc + 32 < spad) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int col = kc + 32 + 4 * u + t;
-            an[u] = (rok && col < s && kc + 32 + 4 * u < spad) ? __ldcg(srow + col) : 0.0;
-          }
-        }
-#else
         double av[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int col = kc + 4 * u + t;
           av[u] = (rok && col < s && kc + 4 * u < spad) ? __ldcg(srow + col) : 0.0;
         }
-#endif
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int k = kc + 4 * u;
@@ -1954,10 +1821,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
             }
           }
         }
-#ifdef HBS_YPF
-#pragma unroll
-        for (int u = 0; u < 8; ++u) av[u] = an[u];
-#endif
       }
       // GEMM2: W2 = W T_p
       double tb[kP / 4][4];
@@ -1981,33 +1844,13 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         for (int c = 2 * t; c < kb; c += 8)
           if (rok) st2(drow + c, ld2(srow + c, c + 1 < kb), c + 1 < kb);
       }
-#ifdef HBS_YPF
-      double2 cn[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = kb + 8 * u + 2 * t;
-        cn[u] = (rok && col < s) ? ld2(srow + col, col + 1 < s) : make_double2(0.0, 0.0);
-      }
-#endif
       for (int nc = kb; nc < spad; nc += 32) {
         double2 cv[4];
-#ifdef HBS_YPF
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cv[u] = cn[u];
-        if (nc + 32 < spad) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int col = nc + 32 + 8 * u + 2 * t;
-            cn[u] = (rok && col < s) ? ld2(srow + col, col + 1 < s) : make_double2(0.0, 0.0);
-          }
-        }
-#else
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int col = nc + 8 * u + 2 * t;
           cv[u] = (rok && col < s) ? ld2(srow + col, col + 1 < s) : make_double2(0.0, 0.0);
         }
-#endif
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int n0 = nc + 8 * u;
@@ -2032,7 +1875,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       }
       __syncwarp();
     }
-#endif
     if (yw == 0 && lane == 0) FUSED_MARK(30 + p);
   }
   // blocked back substitution, row groups shared with group P (which is idle

@@ -306,3 +306,22 @@ def test_oversampled_null_space_matches_reference(n, leaf, r, s):
             level, j = key
             u = f.u_bases[(1 << level) - 1 + j]
             assert np.linalg.norm(u @ u.T - ref.U[level][j] @ ref.U[level][j].T) <= 1e-8, key
+
+
+@pytest.mark.parametrize("k,r,s", [(12, 16, 160), (24, 40, 192)])
+def test_leaf_over_128_rows(k, r, s):
+    """Leaves of 144 rows exceed the 128 TMEM lanes.  s = 160: the fused
+    kernel keeps Y in L2 there (group Y streams it per panel) and in TMEM at
+    the parents; s = 192: Omega^T no longer fits in shared memory and the
+    separate QR / apply-Q kernels run.  All must reproduce the oracle."""
+    n, leaf = 2304, 144
+    truth = O.baseline_generator(n, leaf, k, seed=9)
+    om, ps, y, z = O.samples_from(truth, s, 9)
+    tree = hb.build_tree(n, leaf)
+    assert tree.level_sizes(tree.depth).max() == 144
+    f = gpu_compress((om, ps, y, z), n, leaf, r)
+    ref = O.compress(om, ps, y, z, O.level_bounds(n, tree.depth), r)
+    x = O.gaussian(n, 4, 0, 4)
+    got, want = hb.apply_matrix(f, x), O.apply(ref, x)
+    assert rel(got, want) <= 1e-10
+    assert rel(got, O.apply(truth, x)) <= 1e-10
