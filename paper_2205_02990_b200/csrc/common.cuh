@@ -69,6 +69,13 @@ inline __host__ __device__ int frag_ld(int cols) {
 }
 
 inline __host__ __device__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
+// compile-time forms of round_up / frag_ld (template-specialised kernels)
+constexpr int round_up_c(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int frag_ld_c(int cols) {
+  int ld = (cols + 3) & ~3;
+  while ((ld & 15) != 4) ld += 4;
+  return ld;
+}
 
 // mbarrier helpers (shared::cta).
 HBS_DEV void mbar_init(uint64_t* bar, unsigned count) {

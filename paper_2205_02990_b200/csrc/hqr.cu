@@ -1386,15 +1386,20 @@ HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* ou
 // 128 rows -> TMEM lanes, s <= 256 fp64 columns), so the Y group's three
 // products per panel and the solve read and write Y there instead of
 // round-tripping it through L2.
-template <int MR, bool TM>
+// NF / SF > 0: compile-time box rows and probe count (the launcher runs this
+// specialisation for the boxes with exactly NF rows when s == SF, and the
+// generic kernel (skip_rows = NF) for the others).
+template <int MR, bool TM, int NF = 0, int SF = 0>
 __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   extern __shared__ double smem[];
   const int side = blockIdx.y;
   const int64_t b = blockIdx.x;
   const FusedSide& S = args.side[side];
-  const int nb = box_rows(args.geo, b);
-  const int m = args.s, n = nb, s = args.s;
-  const int lda = args.lda;
+  const int nb_rt = box_rows(args.geo, b);
+  if (NF ? nb_rt != NF : nb_rt == args.skip_rows) return;   // the other launch owns this box
+  const int nb = NF ? NF : nb_rt;
+  const int m = SF ? SF : args.s, n = nb, s = SF ? SF : args.s;
+  const int lda = SF ? frag_ld_c(round_up_c(SF, 32)) : args.lda;
   const int mpad = round_up(m, 32);
   const int npanel = (n + kP - 1) / kP;
   const int64_t rb = args.geo.row_begin[b];
@@ -1892,15 +1897,15 @@ bool fused_fits(int s, int n_max) {
   return n_max <= 16 * kP && d * sizeof(double) <= kMaxSmemBytes;
 }
 
-template <int MR, bool TM>
+template <int MR, bool TM, int NF = 0, int SF = 0>
 static int launch_fused_t(FusedArgs& args, int nsides, cudaStream_t stream) {
   args.lda = frag_ld(round_up(args.s, 32));
   const size_t d = round_up(3 * args.n_max + kP + 35, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
                    (size_t)args.lda * args.n_max;
   const size_t smem = d * sizeof(double);
-  cudaFuncSetAttribute(probe_fused_kernel<MR, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(probe_fused_kernel<MR, TM, NF, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)args.geo.nbox, nsides);
-  probe_fused_kernel<MR, TM><<<grid, 512, smem, stream>>>(args);
+  probe_fused_kernel<MR, TM, NF, SF><<<grid, 512, smem, stream>>>(args);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
@@ -1916,6 +1921,19 @@ static bool fused_tmem_ok(const FusedArgs& args) {
 
 template <int MR>
 static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
+  args.skip_rows = -1;
+#ifndef HBS_NO_FUSED_SPECIAL
+  if constexpr (MR == 6) {
+    // config-4 shape: boxes of exactly 128 rows with s = 192 run a specialised
+    // kernel (compile-time loop bounds); any other boxes of the level follow
+    // in the generic kernel
+    if (fused_tmem_ok(args) && args.s == 192 && args.n_max == 128) {
+      const int rc = launch_fused_t<6, true, 128, 192>(args, nsides, stream);
+      if (rc != kOk) return rc;
+      args.skip_rows = 128;
+    }
+  }
+#endif
   return fused_tmem_ok(args) ? launch_fused_t<MR, true>(args, nsides, stream)
                              : launch_fused_t<MR, false>(args, nsides, stream);
 }

@@ -87,6 +87,7 @@ struct FusedArgs {
   FusedSide side[2];
   int s, n_max, lda;
   double tol;
+  int skip_rows;   // generic kernel: boxes with this many rows were done by a specialised launch (-1: none)
 };
 bool fused_fits(int s, int n_max);
 int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream);
