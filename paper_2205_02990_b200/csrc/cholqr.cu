@@ -376,13 +376,18 @@ HBS_DEV bool cholesky_pass(double* A, int lda, int npad, int rc, double* G, cons
   return true;
 }
 
+// NF / RF > 0: compile-time rows and rank (specialised launch for the boxes
+// with exactly NF rows; the generic launch skips them via skip_rows).
+template <int NF, int RF>
 __global__ void __launch_bounds__(kCT, 2) cholqr_kernel(GeqrfArgs args, int32_t* flag) {
   extern __shared__ double smem[];
   const int side = blockIdx.y;
   const int64_t b = blockIdx.x;
   const GeqrfSide& S = args.side[side];
-  const int nb = box_rows(args.geo, b);
-  const int r = args.n_fixed;
+  const int nb_rt = box_rows(args.geo, b);
+  if (NF ? nb_rt != NF : nb_rt == args.skip_rows) return;   // the other launch owns this box
+  const int nb = NF ? NF : nb_rt;
+  const int r = RF ? RF : args.n_fixed;
   const int rp = round_up(r, 8), rc = round_up(r, 16);
   const int npad = round_up(nb, 8);
   const int lda = frag_ld(rc);            // columns rp .. rc-1 stay zero
@@ -496,15 +501,28 @@ extern "C" int hbs_debug_cq_trace(long long* out) {
 #endif
 }
 
+template <int NF, int RF>
+static int launch_cholqr_t(const GeqrfArgs& args, int nsides, int32_t* flag, size_t smem, cudaStream_t stream) {
+  cudaFuncSetAttribute(cholqr_kernel<NF, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)args.geo.nbox, nsides);
+  cholqr_kernel<NF, RF><<<grid, kCT, smem, stream>>>(args, flag);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
 int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream) {
   const int nmax = args.m_max, r = args.n_fixed;
   if (!cholqr_fits(nmax, r)) return kErrUnsupported;
   const size_t smem = cholqr_smem_bytes(nmax, r);
-  cudaFuncSetAttribute(cholqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)args.geo.nbox, nsides);
-  cholqr_kernel<<<grid, kCT, smem, stream>>>(args, flag);
-  note_launch();
-  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+  args.skip_rows = 0;
+#ifndef HBS_NO_CHOLQR_SPECIAL
+  if (nmax == 128 && r == 64) {   // config-4 shape: compile-time loop bounds
+    const int rc = launch_cholqr_t<128, 64>(args, nsides, flag, smem, stream);
+    if (rc != kOk) return rc;
+    args.skip_rows = 128;
+  }
+#endif
+  return launch_cholqr_t<0, 0>(args, nsides, flag, smem, stream);
 }
 
 }  // namespace hbs

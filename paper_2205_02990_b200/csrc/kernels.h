@@ -53,6 +53,7 @@ struct GeqrfArgs {
   double* gscratch;  // needed when the matrix does not fit in shared memory
   int use_smem;
   const int32_t* only;  // if set: process (box b, side) only when only[side*nbox + b] != 0
+  int skip_rows;        // cholqr generic kernel: boxes with this many rows went to a specialised launch (0: none)
 };
 
 // Blocked Householder (hqr.cu): kFactor also emits the per-panel T and R
