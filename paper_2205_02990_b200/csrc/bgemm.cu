@@ -84,6 +84,21 @@ HBS_DEV void stage_tile(double* s, const double* p, int ld, int i0, int k0, int 
   }
 }
 
+// Interior tile of an aligned operand: 16-byte copies with no bounds checks.
+template <bool KC>
+HBS_DEV void stage_tile_full(double* s, const double* p, int ld, int i0, int k0, int tid) {
+#pragma unroll
+  for (int e = 0; e < (BM * BK / 2) / NT; ++e) {
+    const int idx = tid + e * NT;
+    int i, k;
+    if (KC) { i = idx / (BK / 2); k = 2 * (idx % (BK / 2)); }
+    else { k = idx >> 5; i = 2 * (idx & 31); }
+    const double* src = KC ? p + (int64_t)(i0 + i) * ld + (k0 + k) : p + (int64_t)(k0 + k) * ld + (i0 + i);
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(KC ? &s[i * LDK + k] : &s[k * LDR + i]));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(src));
+  }
+}
+
 // fragment element (row, k) of a staged tile
 template <bool KC>
 HBS_DEV double frag(const double* s, int row, int k) {
@@ -118,9 +133,16 @@ __global__ void __launch_bounds__(NT, BGEMM_MINB) bgemm_kernel(BgemmArgs args) {
   // 16-byte staging when every row start of this box's operands is aligned
   const bool vec = al16(A) && al16(B) && (lda % 2 == 0) && (ldb % 2 == 0);
 
+  // interior tiles of aligned operands stage without bounds checks
+  const bool full = vec && m0 + BM <= M && n0 + BN <= N && (K % BK) == 0;
   auto load = [&](int stage, int k0) {
-    stage_tile<AKC>(As + stage * STAGE, A, lda, m0, k0, M, K, tid, vec);
-    stage_tile<BKC>(Bs + stage * STAGE, B, ldb, n0, k0, N, K, tid, vec);
+    if (full) {
+      stage_tile_full<AKC>(As + stage * STAGE, A, lda, m0, k0, tid);
+      stage_tile_full<BKC>(Bs + stage * STAGE, B, ldb, n0, k0, tid);
+    } else {
+      stage_tile<AKC>(As + stage * STAGE, A, lda, m0, k0, M, K, tid, vec);
+      stage_tile<BKC>(Bs + stage * STAGE, B, ldb, n0, k0, N, K, tid, vec);
+    }
   };
 
   const int warp = tid >> 5, lane = tid & 31;
