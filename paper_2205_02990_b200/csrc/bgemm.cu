@@ -187,6 +187,18 @@ __global__ void __launch_bounds__(NT, BGEMM_MINB) bgemm_kernel(BgemmArgs args) {
   const int ldc0 = args.C0.ld_rows ? rows : args.C0.ld_fixed;
   const double* C0 = has_c0 ? args.C0.p + op_off(args.C0, args.geo, b) : nullptr;
   const bool cvec = al16(C) && (ldc % 2 == 0);
+  if (full && cvec && !has_c0) {   // interior tile, no C0: unpredicated 16-byte stores
+#pragma unroll
+    for (int fi = 0; fi < 4; ++fi)
+#pragma unroll
+      for (int fj = 0; fj < 4; ++fj) {
+        const int i = m0 + wm * 32 + fi * 8 + g;
+        const int j = n0 + wn * 32 + fj * 8 + 2 * t;
+        *reinterpret_cast<double2*>(C + (int64_t)i * ldc + j) =
+            make_double2(args.alpha * acc[fi][fj][0], args.alpha * acc[fi][fj][1]);
+      }
+    return;
+  }
 #pragma unroll
   for (int fi = 0; fi < 4; ++fi)
 #pragma unroll
