@@ -1400,6 +1400,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   const int nb = NF ? NF : nb_rt;
   const int m = SF ? SF : args.s, n = nb, s = SF ? SF : args.s;
   const int lda = SF ? frag_ld_c(round_up_c(SF, 32)) : args.lda;
+  const int nmax = NF ? NF : args.n_max;   // (the specialised launch has n_max == NF)
   const int mpad = round_up(m, 32);
   const int npanel = (n + kP - 1) / kP;
   const int64_t rb = args.geo.row_begin[b];
@@ -1407,11 +1408,11 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   const int g = lane >> 2, t = lane & 3;
 
   double* s_tau = smem;
-  double* s_scale = s_tau + args.n_max;
-  double* s_beta = s_scale + args.n_max;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + args.n_max);   // 32 step barriers
+  double* s_scale = s_tau + nmax;
+  double* s_beta = s_scale + nmax;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_beta + nmax);   // 32 step barriers
   uint64_t* s_ready = s_bar + kP;                                          // 16 panel-ready + 1 R-ready
-  double* G = smem + round_up(3 * args.n_max + kP + 35, 2);
+  double* G = smem + round_up(3 * nmax + kP + 35, 2);
   double* Tscr = G + kP * kLdT;
   double* T = Tscr + 384;
   double* A = T + round_up(kP * kLdT, 2);
