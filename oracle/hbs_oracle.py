@@ -99,6 +99,14 @@ class OracleFactorization:
         return self.U[level][j], self.V[level][j], self.D[level][j]
 
 
+def tree_depth(n, leaf):
+    """Smallest L >= 1 with ceil(n / 2^L) <= leaf (tree.py:80-82)."""
+    depth = 1
+    while (n + (1 << depth) - 1) >> depth > leaf:
+        depth += 1
+    return depth
+
+
 def level_bounds(n, depth):
     """Box row starts per level with the reference split rule (tree.py:84-100)."""
     out = [np.array([0, n], dtype=np.int64)]
@@ -189,7 +197,6 @@ def baseline_generator(n, leaf, k, seed=0, decay=None):
     (leaf rows or 2k rows); leaf D = N(0,1)/sqrt(m) + I; parent D =
     [[0, B1], [B2, 0]]; root [[0, B], [B', 0]]; B = N(0,1)/sqrt(k), or
     Q1 diag(decay^i) Q2^T when `decay` is given (config 4)."""
-    from paper_2205_02990_b200.tree import tree_depth
     depth = tree_depth(n, leaf)
     bounds = level_bounds(n, depth)
     gen = np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy=seed, spawn_key=(STREAM_SYNTHETIC,))))

@@ -1,6 +1,7 @@
 // C-ABI implementation (include/hbs_b200.h): level orchestration of the
 // batched kernels, workspace carving, and the samplers.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include "../../include/hbs_b200.h"
 #include "kernels.h"
@@ -61,6 +62,9 @@ struct LevelWs {
   double* gscratch;
   int32_t* qr_flag;   // 2 x nbox CholeskyQR2 breakdown flags
   bool fused;
+  bool gram;          // Gram / Householder-reconstruction probe factorisation (gram.cu)
+  double* fac[2];     // its output (rows x s per box)
+  int32_t* gflag;     // 2 x nbox: 1 = Householder fallback
   // where the solve results live after factor_and_solve
   const double* Xp[2]; int ldX; int64_t strideX;   // Y Omega^+ / Z Psi^+
   const double* Pp[2]; int ldP; int64_t strideP;   // Y P / Z Q
@@ -70,9 +74,18 @@ size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bo
   const size_t nb = (size_t)nbox;
   const int npanel = (nr + kNB - 1) / kNB;
   const int sides = root_only ? 1 : 2;
-  w.fused = fused_fits(s, nr);
+  // HBS_PROBE_SPLIT=1 (experiments only): separate QR + apply-Q kernels
+  static const bool force_split = std::getenv("HBS_PROBE_SPLIT") != nullptr;
+  w.fused = fused_fits(s, nr) && !force_split;
+  // HBS_GRAM=1: Gram / Householder-reconstruction probe factorisation for the
+  // eligible boxes (experimental; HBS_GRAM=0 or unset: Householder only).
+  // The root needs only Y Omega^+ (unique for any nullity); other levels need
+  // nullity == r for the null-space pick to be basis independent.
+  static const bool use_gram = [] { const char* e = std::getenv("HBS_GRAM"); return e && e[0] == '1'; }();
+  w.gram = w.fused && use_gram && gram_fits(s, nr, root_only ? s - nr : r);
   for (int sd = 0; sd < 2; ++sd) {
     const bool on = sd < sides;
+    w.fac[sd] = (on && w.gram) ? c.take<double>(nb * nr * s) : nullptr;
     // vt doubles as the fused kernel's Y Q buffer (rows x s per box)
     w.vt[sd] = on ? c.take<double>(nb * nr * s) : nullptr;
     w.R[sd] = (on && !w.fused) ? c.take<double>(nb * nr * nr) : nullptr;
@@ -93,6 +106,7 @@ size_t carve_level(Carver& c, LevelWs& w, int64_t nbox, int nr, int s, int r, bo
     w.G1 = w.M3 = w.M4 = w.E1 = w.E2 = nullptr;
     w.qr_flag = nullptr;
   }
+  w.gflag = w.gram ? c.take<int32_t>(2 * nb) : nullptr;
   const bool big_factor = !hqr_fits_smem(s, nr, kGeqrfFactor);
   const bool big_ortho = !root_only && !hqr_fits_smem(nr, r, kGeqrfOrtho);
   w.gscratch = (big_factor || big_ortho)
@@ -147,6 +161,26 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
     }
     w.ldX = s; w.strideX = (int64_t)nr * s;
     w.ldP = s; w.strideP = (int64_t)nr * s;
+    if (w.gram) {
+      // Gram factorisation of every (box, side); the fused kernel applies it
+      // to Y (PRE) and factors the flagged ones by Householder.
+      GramArgs ga;
+      std::memset(&ga, 0, sizeof(ga));
+      ga.geo = geo; ga.s = s; ga.r = s - nr; ga.flag = w.gflag;
+      for (int sd = 0; sd < nsides; ++sd) {
+        GramSide& G = ga.side[sd];
+        G.om = oms[sd]; G.om_c_rb = s;
+        G.fac = w.fac[sd]; G.fac_stride = (int64_t)nr * s;
+        G.t = w.T[sd]; G.t_stride = (int64_t)npanel_f * kNB * kNB;
+        G.status = status + sd * geo.nbox;
+        f.side[sd].fac = w.fac[sd]; f.side[sd].fac_stride = (int64_t)nr * s;
+      }
+      HBS_TRY(launch_gram(ga, nsides, st));
+      f.gflag = w.gflag;
+      f.pre = 1;
+      HBS_TRY(launch_probe_fused(f, nsides, st));
+      f.pre = 0;
+    }
     HBS_TRY(launch_probe_fused(f, nsides, st));
     g_timer.mark(); g_timer.mark(); g_timer.mark();   // (QR, panel factors and apply are one kernel)
     if (root_out) {

@@ -1389,7 +1389,12 @@ HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* ou
 // NF / SF > 0: compile-time box rows and probe count (the launcher runs this
 // specialisation for the boxes with exactly NF rows when s == SF, and the
 // generic kernel (skip_rows = NF) for the others).
-template <int MR, bool TM, int NF = 0, int SF = 0>
+// PRE: the probe factorisation comes from the Gram kernel (gram.cu) in the
+// same layout (fac: V below, R_hh on / above the diagonal; T in S.t): group P
+// only loads it, and group Y applies it to the TMEM rows and solves.  With a
+// Gram flag array, the PRE launch takes the (box, side)s whose flag is 0 and
+// the Householder launch those whose flag is set.
+template <int MR, bool TM, int NF = 0, int SF = 0, bool PRE = false>
 __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   extern __shared__ double smem[];
   const int side = blockIdx.y;
@@ -1397,6 +1402,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   const FusedSide& S = args.side[side];
   const int nb_rt = box_rows(args.geo, b);
   if (NF ? nb_rt != NF : nb_rt == args.skip_rows) return;   // the other launch owns this box
+  if (args.gflag != nullptr && ((args.gflag[(int64_t)side * args.geo.nbox + b] != 0) == PRE)) return;
   const int nb = NF ? NF : nb_rt;
   const int m = SF ? SF : args.s, n = nb, s = SF ? SF : args.s;
   const int lda = SF ? frag_ld_c(round_up_c(SF, 32)) : args.lda;
@@ -1421,7 +1427,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1.
   // Each column is one contiguous Omega row: TMA bulk copies (one per column)
   // completing on an mbarrier when rows are 16-byte aligned, else cp.async.
-  const double* src = S.om + S.om_c_rb * rb;
+  const double* src = PRE ? S.fac + (size_t)b * S.fac_stride : S.om + S.om_c_rb * rb;
   uint64_t* s_load = s_ready + 33;
   const bool bulk = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((lda & 1) == 0) &&
                     ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
@@ -1516,7 +1522,11 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     // ------------------------------------------------------------ group P
     // (physical warps 8..15 = logical 0..7: the arbiter favours high warp ids)
     const int lt = threadIdx.x ^ 256;
-    for (int p = 0; p < npanel; ++p) {
+    if constexpr (PRE) {
+      if (lt == 0)
+        for (int p = 0; p < npanel; ++p) mbar_arrive(&s_ready[p]);   // every panel (and T) is final
+    }
+    for (int p = 0; p < (PRE ? 0 : npanel); ++p) {
       const int j0 = p * kP, nbp = min(kP, n - j0);
       if (p >= 2) mbar_wait(&s_ready[16 + p - 2], 0);   // panels <= p-2 applied to my columns by group Y
       if (lt == 0) FUSED_MARK(21 + 2 * p);
@@ -1536,7 +1546,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       gsync<256>();
       if (lt == 0) { mbar_arrive(&s_ready[p]); FUSED_MARK(1 + 2 * p); }
     }
-    if (lt < 32) {  // sigma screen on diag(R)
+    if (!PRE && lt < 32) {  // sigma screen on diag(R) (PRE: the Gram kernel's status)
       double lo = INFINITY, hi = 0.0;
       for (int j = lt; j < n; j += 32) {
         const double d = fabs(A[j + j * lda]);
@@ -1604,7 +1614,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       const int j0 = p * kP, nbp = min(kP, n - j0), kb = j0 & ~7;
       mbar_wait(&s_ready[p], 0);
       const double* tp = tglob + (size_t)p * kP * kP;
-      if (j0 + 2 * kP < n) {
+      if (!PRE && j0 + 2 * kP < n) {
         block_reflector_apply<256>(A, lda, round_up(m, 8), j0, nbp, tp, true, j0 + 2 * kP, n, kP, 8);
         ysync<256, 2>();
         if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]);
@@ -1898,15 +1908,15 @@ bool fused_fits(int s, int n_max) {
   return n_max <= 16 * kP && d * sizeof(double) <= kMaxSmemBytes;
 }
 
-template <int MR, bool TM, int NF = 0, int SF = 0>
+template <int MR, bool TM, int NF = 0, int SF = 0, bool PRE = false>
 static int launch_fused_t(FusedArgs& args, int nsides, cudaStream_t stream) {
   args.lda = frag_ld(round_up(args.s, 32));
   const size_t d = round_up(3 * args.n_max + kP + 35, 2) + kP * kLdT + 384 + round_up(kP * kLdT, 2) +
                    (size_t)args.lda * args.n_max;
   const size_t smem = d * sizeof(double);
-  cudaFuncSetAttribute(probe_fused_kernel<MR, TM, NF, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(probe_fused_kernel<MR, TM, NF, SF, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)args.geo.nbox, nsides);
-  probe_fused_kernel<MR, TM, NF, SF><<<grid, 512, smem, stream>>>(args);
+  probe_fused_kernel<MR, TM, NF, SF, PRE><<<grid, 512, smem, stream>>>(args);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
@@ -1923,6 +1933,19 @@ static bool fused_tmem_ok(const FusedArgs& args) {
 template <int MR>
 static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
   args.skip_rows = -1;
+  if (args.pre) {   // Gram-factored boxes: Y side only (TMEM rows)
+    if (!fused_tmem_ok(args)) return kErrUnsupported;
+#ifndef HBS_NO_FUSED_SPECIAL
+    if constexpr (MR == 6) {
+      if (args.s == 192 && args.n_max == 128) {
+        const int rc = launch_fused_t<6, true, 128, 192, true>(args, nsides, stream);
+        if (rc != kOk) return rc;
+        args.skip_rows = 128;
+      }
+    }
+#endif
+    return launch_fused_t<MR, true, 0, 0, true>(args, nsides, stream);
+  }
 #ifndef HBS_NO_FUSED_SPECIAL
   if constexpr (MR == 6) {
     // config-4 shape: boxes of exactly 128 rows with s = 192 run a specialised

@@ -82,6 +82,7 @@ struct FusedSide {
   double* t; int64_t t_stride;             // npanel x 32 x 32 compact-WY T blocks
   double* rinv; int64_t rinv_stride;       // npanel x 32 x 32 R diagonal-block inverses
   int32_t* status;
+  const double* fac; int64_t fac_stride;   // PRE: Gram-kernel factorisation (n x s per box)
 };
 struct FusedArgs {
   LevelGeo geo;
@@ -89,9 +90,33 @@ struct FusedArgs {
   int s, n_max, lda;
   double tol;
   int skip_rows;   // generic kernel: boxes with this many rows were done by a specialised launch (-1: none)
+  int pre;                  // 1: apply the Gram factorisation (fac) instead of factoring Omega
+  const int32_t* gflag;     // Gram flags (side*nbox + b): PRE takes flag 0, Householder flag != 0
 };
 bool fused_fits(int s, int n_max);
 int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream);
+
+// ---------------------------------------------------------------- Gram probe factorisation
+// Per (box, side) with nullity s - n == r: Cholesky of Omega Omega^T and
+// Householder reconstruction by a sign-chosen LU (gram.cu).  fac (n x s per
+// box, uniform stride): row j = column j of [R_hh + V1 (strictly lower); V2],
+// the layout the Householder kernel leaves in shared memory; t: compact-WY T
+// of each 32-column panel.  flag[side*nbox + b] = 1 routes the (box, side) to
+// the Householder path (shape, breakdown or doubtful conditioning).
+struct GramSide {
+  const double* om; int64_t om_c_rb;       // Omega rows of box b at om + om_c_rb*row_begin[b], ld = s
+  double* fac; int64_t fac_stride;
+  double* t; int64_t t_stride;
+  int32_t* status;
+};
+struct GramArgs {
+  LevelGeo geo;
+  GramSide side[2];
+  int s, r;
+  int32_t* flag;
+};
+bool gram_fits(int s, int n_max, int r);
+int launch_gram(const GramArgs& args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- apply Q + solve
 // Per (row tile, box, side): Yt <- Y_tile * Q (blocked WY), then

@@ -23,4 +23,4 @@ for idx, level in enumerate(range(tree.depth, 0, -1)):
                   *(m.data_ptr() for m in out), plan.workspace.data_ptr(), plan.workspace_bytes, plan.status.data_ptr(),
                   st, buf), "profiled")
     quad = tuple(m[:g.nbox * 64] for m in out)
-    print(f"L{level:2d} nbox {g.nbox:5d}  fused {buf[0]+buf[1]+buf[2]:7.3f}  basis {buf[3]:6.3f}  disc {buf[4]:6.3f}  lift {buf[5]:6.3f} ms")
+    print(f"L{level:2d} nbox {g.nbox:5d}  probe {buf[0]:7.3f} {buf[1]:7.3f} {buf[2]:7.3f}  basis {buf[3]:6.3f}  disc {buf[4]:6.3f}  lift {buf[5]:6.3f} ms")
