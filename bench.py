@@ -41,30 +41,7 @@ CONFIGS = {
     "c5": (1 << 22, 128, 256, 384, 128, None),
 }
 METRIC = "HBS compress-from-samples rows/s (fp64) at N=2^20,k=64"
-PHASES = ("probe_qr", "panel_factors", "apply_q_solve", "basis_qr", "discrepancy_gemm", "lift_gemm")
-
-
-def canonical_phase_flops(n, s, r):
-    """Canonical Householder flop model per box, by phase."""
-    return {
-        "probe_qr": 2 * (2 * n * n * (s - n / 3)),
-        "panel_factors": 0.0,
-        "apply_q_solve": 2 * ((4 * n * n * s - 2 * n ** 3) + n ** 3),
-        "basis_qr": 2 * (4 * r * r * (n - r / 3)),
-        "discrepancy_gemm": 12 * r * n * n,
-        "lift_gemm": 4 * n * n * s + 8 * r * n * s,
-    }
-
-
-def canonical_total_flops(tree, s, r):
-    total = 0.0
-    for level in range(tree.depth, 0, -1):
-        sizes = tree.level_sizes(level) if level == tree.depth else np.full(1 << level, 2 * r)
-        for n in np.unique(sizes):
-            total += int((sizes == n).sum()) * sum(canonical_phase_flops(int(n), s, r).values())
-    n = 2 * r
-    total += 2 * n * n * (s - n / 3) + 4 * n * n * s - n ** 3
-    return total
+from paper_2205_02990_b200.roofline import PHASES, canonical_phase_flops, canonical_total_flops  # noqa: E402
 
 
 def fused_traffic():
@@ -78,10 +55,12 @@ def fused_traffic():
 
 
 def fp64_peak():
-    path = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    path = os.path.join(ROOT, "profiles", "fp64_peaks_r02.json")
     with open(path) as fh:
-        return float(json.load(fh)["fp64_peak_tflops"]), "measured: DMMA m8n8k4 microbenchmark " \
-            "(tools/fp64_peak.cu, profiles/fp64_peaks_r01.json; cuBLAS DGEMM 8192^3 = 35.5 TF/s)"
+        d = json.load(fh)
+    return float(d["fp64_peak_tflops"]), ("measured: best DMMA rate of tools/fp64_peak.cu at "
+                                          f"{d['clocks']['sm_mhz']:.0f} MHz, no throttle reasons "
+                                          "(profiles/fp64_peaks_r02.json); NVIDIA spec 40 TF/s")
 
 
 class ClockSampler:
@@ -125,45 +104,99 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_rate(cfg, n_sample, repeats=1):
-    """The oracle port of the reference (bitwise-identical numerics) on a
-    bounded sample of the workload: same k, r, leaf, s; N = n_sample."""
-    from oracle import hbs_oracle as O
-    _, k, leaf, s, r, decay = cfg
-    g = O.baseline_generator(n_sample, leaf, k, seed=0, decay=decay)
-    om, ps, y, z = O.samples_from(g, s, 0)
-    rates = []
-    for _ in range(repeats):
+def reference_module():
+    """The unmodified reference package: baseline/_ref (pip-installed from
+    /root/reference, travels to the GPU box) or /root/reference/pkg/src; None
+    when neither exists (the oracle port is used instead)."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isfile(os.path.join(path, "hbs", "__init__.py")):
+            os.environ.setdefault("HBS_THREADS", str(os.cpu_count() or 1))
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            import hbs
+            return hbs
+    return None
+
+
+class ReferenceSample:
+    """A bounded sample of the workload for the reference CPU path: the
+    section-8(d) operator at N = n_sample (same k, r, leaf, s; rows/s is
+    N-independent at fixed shape) and its seeded
+    samples, drawn through the reference's own draw_samples / hbs_oracle."""
+
+    def __init__(self, cfg, n_sample):
+        from oracle import hbs_oracle as O
+        _, k, leaf, s, r, decay = cfg
+        self.n, self.r = n_sample, r
+        self.truth = O.baseline_generator(n_sample, leaf, k, seed=0, decay=decay)
+        self.hbs = reference_module()
+        if self.hbs is not None:
+            from hbs import operators
+            f = self.truth
+            u, v, d = {}, {}, {}
+            for level in range(1, f.depth + 1):
+                for j in range(1 << level):
+                    nid = (1 << level) - 1 + j
+                    u[nid], v[nid], d[nid] = f.U[level][j], f.V[level][j], f.D[level][j]
+            self.tree = self.hbs.build_tree(n_sample, leaf)
+            ref_f = self.hbs.HbsFactorization(self.tree, k, u, v, d, f.root)
+            self.samples = self.hbs.draw_samples(operators.hbs_oracle(ref_f), s, 0)
+            self.config = self.hbs.CompressionConfig(rank=r, leaf_threshold=leaf, probes=s)
+            self.kind = "reference"
+        else:
+            self.quad = O.samples_from(self.truth, s, 0)
+            self.kind = "port"
+
+    def step(self):
+        """One timed compress_from_samples of the sample (seconds)."""
         t0 = time.perf_counter()
-        O.compress(om, ps, y, z, g.bounds, r)
-        rates.append(n_sample / (time.perf_counter() - t0))
-    return rates
+        if self.kind == "reference":
+            self.hbs.compress_from_samples(self.samples, self.tree, self.config)
+        else:
+            from oracle import hbs_oracle as O
+            O.compress(*self.quad, self.truth.bounds, self.r)
+        return time.perf_counter() - t0
+
+    def describe(self, cores):
+        what = ("the unmodified reference hbs.compress_from_samples (baseline/_ref)" if self.kind == "reference"
+                else "the oracle port of the reference compress_from_samples (bitwise-identical numerics)")
+        return (f"{what} on the config's shape at N={self.n} (rows/s is N-independent at fixed k, leaf, s); "
+                f"numpy/OpenBLAS with HBS_THREADS={cores}, effectively single-core")
 
 
 def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores; rank 0 only.  Each step is one compress of the bounded sample;
+    ms_per_step is what was timed."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    n_sample = args.ref_sample
+    smp = ReferenceSample(cfg, min(args.ref_sample, cfg[0]))
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, n_sample)
-    rates = []
-    for _ in range(args.steps):
-        rates += cpu_reference_rate(cfg, n_sample)
-    value = float(np.mean(rates))
-    N = cfg[0]
+        smp.step()
+    times = [smp.step() for _ in range(args.steps)]
+    value = smp.n / float(np.mean(times))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * N / value,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "n_timed": len(times), "sample_rows": smp.n, "best_rows_per_s": smp.n / min(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(args, cfg, world),
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle port of compress_from_samples on the config-4 shape at N={n_sample} "
-                                   f"(rows/s is N-independent at fixed k, leaf, s); numpy/OpenBLAS with "
-                                   f"{cores} threads available, effectively single-core"},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": smp.kind,
+                         "sample": smp.describe(cores)},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(args, cfg):
+    """The reference CPU path on a bounded sample (rank 0, N = 1): best of 3."""
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    smp = ReferenceSample(cfg, min(args.cpu_sample, cfg[0]))
+    times = [smp.step() for _ in range(3)]
+    return {"value": smp.n / min(times), "unit": "rows/s", "cores": cores, "kind": smp.kind,
+            "sample": smp.describe(cores) + f"; best of 3, {time.perf_counter() - t0:.1f} s incl. input generation"}
 
 
 def run_distributed(args, cfg, world, rank, dev):
@@ -256,8 +289,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None, help="override N (rows per GPU)")
-    ap.add_argument("--ref-sample", type=int, default=1 << 14)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 15)
+    ap.add_argument("--ref-sample", type=int, default=1 << 13, help="rows per reference step (bounded sample)")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 13)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -383,13 +416,7 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        n_cpu = min(args.cpu_sample, N)
-        t0 = time.perf_counter()
-        rate = cpu_reference_rate(cfg, n_cpu)[0]
-        cpu = {"value": rate, "unit": "rows/s", "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": f"oracle port of the reference compress_from_samples (bitwise-identical numerics) on the "
-                         f"{args.config} shape at N={n_cpu}; numpy/OpenBLAS, all host threads available, "
-                         f"effectively single-core; {time.perf_counter() - t0:.1f} s incl. input generation"}
+        cpu = cpu_baseline_leg(args, cfg)
 
     if rank == 0:
         line = {

@@ -429,7 +429,10 @@ def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, 
     for lv, (hu, hv, hd) in hosts.items():
         f._host[(lv, "u")], f._host[(lv, "v")], f._host[(lv, "d")] = hu.numpy(), hv.numpy(), hd.numpy()
     f._host["root"] = top.root.cpu().numpy()
-    f._host_keepalive = (hosts, dq, plans)
+    # (the device copies of the samples and the plans' workspaces are freed
+    # here: the synchronize above ordered every use of them)
+    f._host_keepalive = hosts
+    del dq, plans, top
     return f
 
 

@@ -84,80 +84,136 @@ HBS_DEV double rcp_g(double a) {
 }
 
 // Cholesky of the diagonal block Bd (upper triangle = current Schur
-// complement) in place; rd[j] = R_jj, ri[j] = 1 / R_jj.  One warp; lane k
-// (and its mirror k + 16) owns column k.  Returns false on breakdown.
-HBS_DEV bool chol16(double* Bd, double* rd, double* ri, double* row, double floor_) {
-  const int lane = threadIdx.x & 31, kc = lane & 15;
+// complement) in place, row-owned: lane i (and its mirror i + 16) holds row i
+// in registers and row j of R is broadcast by shuffles.  rd[j] = R_jj.  Then
+// Ri = R_oo^{-1} (upper; swizzled block).  One warp; false on breakdown.
+HBS_DEV bool chol16_inv(double* Bd, double* rd, double* Ri, double floor_) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
   double c[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) c[i] = Bd[bsw(i, kc)];
+  for (int k = 0; k < 16; ++k) c[k] = (k >= i) ? Bd[bsw(i, k)] : 0.0;
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const double d = __shfl_sync(0xffffffffu, c[j], j);
     ok = ok && (d > floor_) && (d < 1e300);
     const double rs = rsqrt_g(d);
-    c[j] = (kc == j) ? d * rs : (kc > j ? c[j] * rs : 0.0);
-    if (lane == j) { rd[j] = d * rs; ri[j] = rs; }
-    row[kc] = c[j];
-    __syncwarp();
-    const double2* r2 = reinterpret_cast<const double2*>(row);
+    if (i == j) {
 #pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      if (2 * h + 1 > j) {
-        const double2 v = r2[h];
-        if (2 * h > j) c[2 * h] = (2 * h <= kc) ? fma(-v.x, c[j], c[2 * h]) : c[2 * h];
-        c[2 * h + 1] = (2 * h + 1 <= kc) ? fma(-v.y, c[j], c[2 * h + 1]) : c[2 * h + 1];
-      }
+      for (int k = 0; k < 16; ++k)
+        if (k >= j) c[k] *= rs;
     }
-    __syncwarp();
+    double rj[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k >= j) rj[k] = __shfl_sync(0xffffffffu, c[k], j);
+    double rji = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k > j && k == i) rji = rj[k];
+    if (i > j) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k > j && k >= i) c[k] = fma(-rji, rj[k], c[k]);
+    }
   }
   if (lane < 16) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i <= kc) Bd[bsw(i, kc)] = c[i];
+    for (int k = 0; k < 16; ++k)
+      if (k >= i) Bd[bsw(i, k)] = c[k];
+    double di = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k == i) di = c[k];
+    rd[i] = di;
+  }
+  __syncwarp();
+  // row i of R^{-1}: x R = e_i (forward over columns, right-looking)
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = (k == i) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    x[k] *= rcp_g(Bd[bsw(k, k)]);
+#pragma unroll
+    for (int l = 0; l < 16; ++l)
+      if (l > k) x[l] = fma(-x[k], Bd[bsw(k, l)], x[l]);
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Ri[bsw(i, k)] = x[k];
   }
   return __all_sync(0xffffffffu, ok);
 }
 
 // LU of the 16 x 16 diagonal block of M at (ko, ko) with the Householder sign
-// rule: pivot row j first loses s_j R(ko + j, ko + j:) with s_j = -sign of its
-// current diagonal, so |pivot| = |a| + R_jj.  Unit lower L below, U' on and
-// above the diagonal; sg[j] = s_j, pinv[j] = 1 / U'_jj.  One warp.
-HBS_DEV void lu16(double* X, int ko, const double* Rd, double* sg, double* pinv, double* row) {
-  const int lane = threadIdx.x & 31, kc = lane & 15;
-  double c[16];
-  double* col = X + ko + (ko + kc) * kLdX;
+// rule, row-owned: pivot row j first loses s_j R(ko + j, ko + j:) with s_j =
+// -sign of its current diagonal (|pivot| = |a| + R_jj), then is broadcast by
+// shuffles.  Unit lower L below, U' on / above the diagonal (in X);
+// sg[j] = s_j; Li = L^{-1} (unit lower) and Ui = U'^{-1} (upper), swizzled.
+HBS_DEV void lu16_inv(double* X, int ko, const double* Rd, double* sg, double* Li, double* Ui) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  double c[16], rr[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) c[i] = col[i];
+  for (int k = 0; k < 16; ++k) {
+    c[k] = X[(ko + i) + (ko + k) * kLdX];
+    rr[k] = (k >= i) ? Rd[bsw(i, k)] : 0.0;
+  }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const double a = __shfl_sync(0xffffffffu, c[j], j);
-    const double sj = a >= 0.0 ? -1.0 : 1.0;
-    if (kc >= j) c[j] = fma(-sj, Rd[bsw(j, kc)], c[j]);
-    const double d = __shfl_sync(0xffffffffu, c[j], j);
-    const double dinv = rcp_g(d);
-    if (lane == j) { sg[j] = sj; pinv[j] = dinv; }
-    if (kc == j) {
+    double dinv = 0.0;
+    if (i == j) {
+      const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i > j) c[i] *= dinv;
+      for (int k = 0; k < 16; ++k)
+        if (k >= j) c[k] = fma(-sj, rr[k], c[k]);
+      dinv = rcp_g(c[j]);
+      if (lane == j) sg[j] = sj;
     }
-    if (lane == j) {
+    dinv = __shfl_sync(0xffffffffu, dinv, j);
+    double uj[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) row[i] = c[i];
-    }
-    __syncwarp();
-    if (kc > j) {
+    for (int k = 0; k < 16; ++k)
+      if (k > j) uj[k] = __shfl_sync(0xffffffffu, c[k], j);
+    if (i > j) {
+      const double l = c[j] * dinv;
+      c[j] = l;
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i > j) c[i] = fma(-row[i], c[j], c[i]);
+      for (int k = 0; k < 16; ++k)
+        if (k > j) c[k] = fma(-l, uj[k], c[k]);
     }
-    __syncwarp();
   }
   if (lane < 16) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) col[i] = c[i];
+    for (int k = 0; k < 16; ++k) X[(ko + i) + (ko + k) * kLdX] = c[k];
+  }
+  __syncwarp();
+  // lanes 0..15: column i of L^{-1} (unit lower); lanes 16..31: column i of U'^{-1}
+  double z[16];
+  if (lane < 16) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m)
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q > m && m >= i) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) Li[bsw(m, i)] = z[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 15; m >= 0; --m) {
+      if (m <= i) {
+        z[m] *= rcp_g(X[(ko + m) + (ko + m) * kLdX]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < m) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 16; ++m) Ui[bsw(m, i)] = z[m];
   }
 }
 
@@ -179,16 +235,16 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
   const int nb = n >> 4;
   double* X = smem;                                  // M (n x n, col-major, ld kLdX)
   double* Yr = X + kGN * kLdX;                       // chunk buffers | G / R blocks
-  double* Uinv = Yr + 2 * kGN * kLdC;                // inverses of U' diagonal blocks
-  double* rdiag = Uinv + 8 * kBlk;                   // R_jj
-  double* rinvd = rdiag + kGN;                       // 1 / R_jj
-  double* sg = rinvd + kGN;                          // Householder signs s_j
-  double* pinv = sg + kGN;                           // 1 / U'_jj
-  double* rowbuf = pinv + kGN;                       // 16 (+pad)
-  int* s_ok = reinterpret_cast<int*>(rowbuf + 32);
+  double* Uinv = Yr + 2 * kGN * kLdC;                // inverses of U' diagonal blocks (V2)
+  double* Rinv = Uinv + 8 * kBlk;                    // R_oo^{-1} of the current Cholesky block
+  double* Linv = Rinv + kBlk;                        // L_oo^{-1} of the current LU block
+  double* rdiag = Linv + kBlk;                       // R_jj
+  double* sg = rdiag + kGN;                          // Householder signs s_j
+  int* s_ok = reinterpret_cast<int*>(sg + kGN);
   const GR Gm{Yr, nb};
 
   const double* om = S.om + S.om_c_rb * args.geo.row_begin[b];
+  GR_MARK(0);
 
   // ---------------------------------------------------------------- G = Omega Omega^T
   // Omega streams through two 32-column chunk buffers; the columns < n also
@@ -261,57 +317,102 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
     }
   }
   __syncthreads();
-  GR_MARK(0);
+  GR_MARK(1);
 
-  // ---------------------------------------------------------------- Cholesky G = R^T R
+  // ---------------------------------------------------------------- Cholesky and LU, pipelined
+  // Iteration it: Cholesky block o_c = it of G = R^T R, and LU block
+  // o_l = it - 1 of M = Omega_1^T - S R (it needs R's block row o_l, final
+  // since iteration it - 1).  (A) warp 0 factors / inverts R's diagonal
+  // block, warp 1 the LU diagonal block (L^{-1}, U'^{-1}); (B) block row of
+  // R, U12 = L^{-1} (M12 - S R12) and L21 = M21 U'^{-1} on the tensor cores;
+  // (C) both trailing updates.
   double gmax = 0.0;
   for (int j = lane; j < n; j += 32) gmax = fmax(gmax, Gm.at(j, j));
   gmax = warp_max(gmax);
   const double floor_ = 1e-24 * gmax;
-  for (int o = 0; o < nb; ++o) {
-    if (warp == 0) {
-      const bool ok = chol16(Gm.blk(o, o), rdiag + 16 * o, rinvd + 16 * o, rowbuf, floor_);
-      if (threadIdx.x == 0) *s_ok = ok;
+  for (int it = 0; it <= nb; ++it) {
+    const int oc = it, ol = it - 1, kl = 16 * ol;
+    if (warp == 0 && oc < nb) {
+      const bool ok = chol16_inv(Gm.blk(oc, oc), rdiag + 16 * oc, Rinv, floor_);
+      if (lane == 0) *s_ok = ok;
+    } else if (warp == 1 && ol >= 0) {
+      lu16_inv(X, kl, Gm.blk(ol, ol), sg + kl, Linv, Uinv + ol * kBlk);
     }
     __syncthreads();
     if (!*s_ok) {
       if (threadIdx.x == 0) *myflag = 1;
       return;
     }
-    const int m = n - 16 * (o + 1);
-    if (m > 0) {
-      // block row o: R(o, c) = R_oo^{-T} G(o, c), one thread per column
-      if (threadIdx.x < m) {
-        const int cc = 16 * (o + 1) + threadIdx.x;
-        double* bc = Gm.blk(o, cc >> 4);
-        const double* bd = Gm.blk(o, o);
-        const int cl = cc & 15;
-        double x[16];
+    // (B) units of 16 x 8 (Cholesky / U12: one block column half) or 8 x 16 (L21)
+    const int nbc = oc < nb ? nb - oc - 1 : 0;     // Cholesky block columns right of oc
+    const int nbl = ol >= 0 ? nb - ol - 1 : 0;     // LU blocks right of / below ol
+    const int ub = 2 * nbc + 4 * nbl;
+    for (int u = warp; u < ub; u += kGT / 32) {
+      if (u < 2 * nbc) {                           // R(oc, cb) = R_oo^{-T} G(oc, cb)
+        const int cb = oc + 1 + (u >> 1), fj = u & 1;
+        double* bc = Gm.blk(oc, cb);
+        double acc2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = bc[bsw(i, cl)];
+        for (int k = 0; k < 16; k += 4) {
+          const double bv = bc[bsw(k + t, 8 * fj + g)];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          x[i] *= rinvd[16 * o + i];
-#pragma unroll
-          for (int l = 0; l < 16; ++l)
-            if (l > i) x[l] = fma(-bd[bsw(i, l)], x[i], x[l]);
+          for (int fi = 0; fi < 2; ++fi) dmma8x8x4(acc2[fi][0], acc2[fi][1], Rinv[bsw(k + t, 8 * fi + g)], bv);
         }
+        __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) bc[bsw(i, cl)] = x[i];
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) bc[bsw(8 * fi + g, 8 * fj + 2 * t + e)] = acc2[fi][e];
+      } else if (u < 2 * nbc + 2 * nbl) {         // U12 = L^{-1} (M12 - S R12)
+        const int v = u - 2 * nbc, cb = ol + 1 + (v >> 1), fj = v & 1;
+        const double* rb2 = Gm.blk(ol, cb);
+        const int col = 16 * cb + 8 * fj + g;
+        double acc2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          const double bv = fma(-sg[kl + k + t], rb2[bsw(k + t, 8 * fj + g)], X[(kl + k + t) + col * kLdX]);
+#pragma unroll
+          for (int fi = 0; fi < 2; ++fi) dmma8x8x4(acc2[fi][0], acc2[fi][1], Linv[bsw(8 * fi + g, k + t)], bv);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) X[(kl + 8 * fi + g) + (16 * cb + 8 * fj + 2 * t + e) * kLdX] = acc2[fi][e];
+      } else {                                     // L21 = M21 U'^{-1}
+        const int v = u - 2 * nbc - 2 * nbl, rbk = ol + 1 + (v >> 1), fi = v & 1;
+        const int row = 16 * rbk + 8 * fi + g;
+        const double* ui = Uinv + ol * kBlk;
+        double acc2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          const double av = X[row + (kl + k + t) * kLdX];
+#pragma unroll
+          for (int fj = 0; fj < 2; ++fj) dmma8x8x4(acc2[fj][0], acc2[fj][1], av, ui[bsw(k + t, 8 * fj + g)]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int fj = 0; fj < 2; ++fj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) X[row + (kl + 8 * fj + 2 * t + e) * kLdX] = acc2[fj][e];
       }
-      __syncthreads();
-      // trailing: G(bi, bj) -= R(o, bi)^T R(o, bj), o < bi <= bj (8 x 8 tiles)
-      const int mb = nb - o - 1;
-      const int units = mb * (mb + 1) / 2 * 4;
-      for (int u = warp; u < units; u += kGT / 32) {
+    }
+    __syncthreads();
+    // (C) trailing updates, 8 x 8 tiles: Cholesky (upper block triangle) then LU (square)
+    const int mb = nbc;
+    const int uc = mb * (mb + 1) / 2 * 4;
+    const int mt = 2 * nbl;
+    const int ut = uc + mt * mt;
+    for (int u = warp; u < ut; u += kGT / 32) {
+      if (u < uc) {
         int q = u >> 2, bi = 0;
         while (q >= mb - bi) { q -= mb - bi; ++bi; }
-        const int bj = bi + q + o + 1;
-        bi += o + 1;
+        const int bj = bi + q + oc + 1;
+        bi += oc + 1;
         const int fi = (u >> 1) & 1, fj = u & 1;
         if (bi == bj && fi > fj) continue;
-        const double* ra = Gm.blk(o, bi);
-        const double* rb2 = Gm.blk(o, bj);
+        const double* ra = Gm.blk(oc, bi);
+        const double* rb2 = Gm.blk(oc, bj);
         double* cb = Gm.blk(bi, bj);
         double c0 = cb[bsw(8 * fi + g, 8 * fj + 2 * t)], c1 = cb[bsw(8 * fi + g, 8 * fj + 2 * t + 1)];
 #pragma unroll
@@ -319,9 +420,20 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
           dmma8x8x4(c0, c1, -ra[bsw(k + t, 8 * fi + g)], rb2[bsw(k + t, 8 * fj + g)]);
         cb[bsw(8 * fi + g, 8 * fj + 2 * t)] = c0;
         cb[bsw(8 * fi + g, 8 * fj + 2 * t + 1)] = c1;
+      } else {
+        const int v = u - uc;
+        const int c0r = kl + 16 + 8 * (v / mt), d0 = kl + 16 + 8 * (v % mt);
+        double* cp = X + (c0r + g) + (d0 + 2 * t) * kLdX;
+        double c0 = cp[0], c1 = cp[kLdX];
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma8x8x4(c0, c1, -X[(c0r + g) + (kl + k + t) * kLdX], X[(kl + k + t) + (d0 + g) * kLdX]);
+        cp[0] = c0;
+        cp[kLdX] = c1;
       }
-      __syncthreads();
     }
+    __syncthreads();
+    if (it == nb - 1) GR_MARK(2);
   }
   // screen: the Gram squares cond(Omega); route doubtful boxes to Householder
   if (warp == 0) {
@@ -332,155 +444,98 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
     if (lane == 0) *s_ok = (hi > 0.0) && isfinite(hi) && lo >= kFallbackRatio * hi;
   }
   __syncthreads();
-  GR_MARK(1);
+  GR_MARK(3);
   if (!*s_ok) {
     if (threadIdx.x == 0) *myflag = 1;
     return;
   }
 
-  // ---------------------------------------------------------------- LU of M = Omega_1^T - S R
-  for (int o = 0; o < nb; ++o) {
-    const int ko = 16 * o;
-    if (warp == 0) lu16(X, ko, Gm.blk(o, o), sg + ko, pinv + ko, rowbuf);
-    __syncthreads();
-    const int m = n - ko - 16;
-    if (m > 0) {
-      if (threadIdx.x < m) {
-        // U12: column c of the block row, minus s_i R(ko + i, c), then L11^{-1}
-        const int cc = ko + 16 + threadIdx.x;
-        const double* rb2 = Gm.blk(o, cc >> 4);
-        const int cl = cc & 15;
-        double x[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = fma(-sg[ko + i], rb2[bsw(i, cl)], X[(ko + i) + cc * kLdX]);
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-#pragma unroll
-          for (int l = 0; l < 16; ++l)
-            if (l > i) x[l] = fma(-X[(ko + l) + (ko + i) * kLdX], x[i], x[l]);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) X[(ko + i) + cc * kLdX] = x[i];
-      } else if (threadIdx.x >= 256 && threadIdx.x < 256 + m) {
-        // L21: row c of the block column times U11^{-1}
-        const int cr = ko + 16 + (threadIdx.x - 256);
-        double y[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) y[j] = X[cr + (ko + j) * kLdX];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          y[j] *= pinv[ko + j];
-#pragma unroll
-          for (int l = 0; l < 16; ++l)
-            if (l > j) y[l] = fma(-X[(ko + j) + (ko + l) * kLdX], y[j], y[l]);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) X[cr + (ko + j) * kLdX] = y[j];
-      }
-      __syncthreads();
-      // trailing M(c, d) -= L(c, ko:ko+16) U(ko:ko+16, d), 8 x 8 tiles
-      const int mt = m >> 3;
-      for (int u = warp; u < mt * mt; u += kGT / 32) {
-        const int c0r = ko + 16 + 8 * (u / mt), d0 = ko + 16 + 8 * (u % mt);
-        double* cp = X + (c0r + g) + (d0 + 2 * t) * kLdX;
-        double c0 = cp[0], c1 = cp[kLdX];
-#pragma unroll
-        for (int k = 0; k < 16; k += 4)
-          dmma8x8x4(c0, c1, -X[(c0r + g) + (ko + k + t) * kLdX], X[(ko + k + t) + (d0 + g) * kLdX]);
-        cp[0] = c0;
-        cp[kLdX] = c1;
-      }
-      __syncthreads();
-    }
-  }
-  GR_MARK(2);
-
-  // inverses of U' diagonal blocks (for V2), one warp per block
-  if (warp < nb) {
-    const int kc = lane & 15, ko = 16 * warp;
-    double z[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = (i == kc) ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = 15; l >= 0; --l) {
-      z[l] *= pinv[ko + l];
-#pragma unroll
-      for (int i = 0; i < 15; ++i)
-        if (i < l) z[i] = fma(-X[(ko + i) + (ko + l) * kLdX], z[l], z[i]);
-    }
-    if (lane < 16) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) Uinv[warp * kBlk + bsw(i, kc)] = z[i];
-    }
-  }
-  __syncthreads();
-
   double* fac = S.fac + (size_t)b * S.fac_stride;   // n x s, row j = column j of [R_hh + V1; V2]
   if (warp < 8) {
     // ------------------------------------------------------------ V2 = Omega_2^T U'^{-1}
+    // right-looking block forward substitution, 8 rows per warp: the
+    // accumulators of every column block start as Omega_2^T (loads issued up
+    // front) and lose V2(:, bb) U'(bb, cc) as soon as block bb is final.
     for (int rb = warp; 8 * rb < r; rb += 8) {
       const int q = 8 * rb + g;
       const bool qok = q < r;
-      double vf[8][4];
+      double acc[8][2][2];
+#pragma unroll
+      for (int bb = 0; bb < 8; ++bb)
+#pragma unroll
+        for (int f = 0; f < 2; ++f)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 16 * bb + 8 * f + 2 * t + e;
+            acc[bb][f][e] = (bb < nb && qok) ? __ldg(om + (int64_t)col * s + n + q) : 0.0;
+          }
 #pragma unroll
       for (int bb = 0; bb < 8; ++bb) {
         if (bb < nb) {
-        double a[4];
+          const double* ui = Uinv + bb * kBlk;
+          double v[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) a[kk] = qok ? __ldg(om + (int64_t)(16 * bb + 4 * kk + t) * s + n + q) : 0.0;
-        if (bb > 0) {
-          double ac[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          for (int kk = 0; kk < 16; kk += 4) {
+            const double a = cfrag_to_afrag<2>(acc[bb], kk, lane);
 #pragma unroll
-          for (int pa = 0; pa < 8; ++pa) {
-            if (pa < bb) {
+            for (int f = 0; f < 2; ++f) dmma8x8x4(v[f][0], v[f][1], a, ui[bsw(kk + t, 8 * f + g)]);
+          }
+          if (qok) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
+            for (int f = 0; f < 2; ++f)
 #pragma unroll
-              for (int f = 0; f < 2; ++f)
-                dmma8x8x4(ac[f][0], ac[f][1], vf[pa][kk], X[(16 * pa + 4 * kk + t) + (16 * bb + 8 * f + g) * kLdX]);
+              for (int e = 0; e < 2; ++e) fac[(size_t)(16 * bb + 8 * f + 2 * t + e) * s + n + q] = v[f][e];
+          }
+          double va[4];
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 4) va[kk / 4] = -cfrag_to_afrag<2>(v, kk, lane);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            if (cc > bb && cc < nb) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+                  dmma8x8x4(acc[cc][f][0], acc[cc][f][1], va[kk], X[(16 * bb + 4 * kk + t) + (16 * cc + 8 * f + g) * kLdX]);
             }
           }
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) a[kk] -= cfrag_to_afrag<2>(ac, 4 * kk, lane);
-        }
-        double ac[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        const double* ui = Uinv + bb * kBlk;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-          for (int f = 0; f < 2; ++f) dmma8x8x4(ac[f][0], ac[f][1], a[kk], ui[bsw(4 * kk + t, 8 * f + g)]);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) vf[bb][kk] = cfrag_to_afrag<2>(ac, 4 * kk, lane);
-        if (qok) {
-#pragma unroll
-          for (int f = 0; f < 2; ++f)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) fac[(size_t)(16 * bb + 8 * f + 2 * t + e) * s + n + q] = ac[f][e];
-        }
         }
       }
     }
-  } else if (warp < 12) {
+  } else {
     // ------------------------------------------------------------ T of panel p
+    // lane i: row i of Z = U'_pp R_pp^{-1} (right-looking forward substitution),
+    // then (Z S) V1,pp^{-T} in place; T_p = -result.
     const int p = warp - 8, j0 = 32 * p;
     if (j0 < n) {
       const int nbp = min(32, n - j0), i = lane;
-      double z[32];   // row i of U'_pp R_pp^{-1}, then (in place) of -T_p
+      const int bo = j0 >> 4;
+      const double* Rb[2][2] = {{Gm.blk(bo, bo), Gm.blk(bo, min(bo + 1, nb - 1))},
+                                {Gm.blk(min(bo + 1, nb - 1), min(bo + 1, nb - 1)), nullptr}};
+      double z[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        double a = (j >= i && j < nbp && i < nbp) ? X[(j0 + i) + (j0 + j) * kLdX] : 0.0;
+      for (int j = 0; j < 32; ++j) z[j] = (j >= i && j < nbp && i < nbp) ? X[(j0 + i) + (j0 + j) * kLdX] : 0.0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < j) a = fma(-z[k], (j < nbp) ? Gm.at(j0 + k, j0 + j) : 0.0, a);
-        z[j] = (j < nbp) ? a * rinvd[j0 + j] : 0.0;
+      for (int k = 0; k < 32; ++k) {
+        if (k < nbp) {
+          const double* rk = Rb[k >> 4][0];
+          z[k] *= rcp_g(rk[bsw(k & 15, k & 15)]);
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            if (l > k && l < nbp) {
+              const double* rbl = (k >> 4) == (l >> 4) ? Rb[k >> 4][0] : Rb[0][1];
+              z[l] = fma(-z[k], rbl[bsw(k & 15, l & 15)], z[l]);
+            }
+        }
       }
-      // (Z S) V1^{-T}: forward substitution over j, in place (z[k < j] final)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        double a = (j < nbp) ? z[j] * sg[j0 + j] : 0.0;
+      for (int k = 0; k < 32; ++k) {
+        if (k < nbp) {
+          z[k] *= sg[j0 + k];
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < j) a = fma(-z[k], (j < nbp) ? X[(j0 + j) + (j0 + k) * kLdX] : 0.0, a);
-        z[j] = a;
+          for (int l = 0; l < 32; ++l)
+            if (l > k && l < nbp) z[l] = fma(-z[k], X[(j0 + l) + (j0 + k) * kLdX], z[l]);
+        }
       }
       double* tp = S.t + (size_t)b * S.t_stride + (size_t)p * kNB * kNB + (size_t)i * kNB;
 #pragma unroll
@@ -497,11 +552,11 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
     *myflag = 0;
     S.status[b] = kBoxOk;
   }
-  GR_MARK(3);
+  GR_MARK(4);
 }
 
 size_t gram_smem_bytes() {
-  return ((size_t)kGN * kLdX + 2 * kGN * kLdC + 8 * kBlk + 4 * kGN + 40) * sizeof(double);
+  return ((size_t)kGN * kLdX + 2 * kGN * kLdC + 10 * kBlk + 2 * kGN + 8) * sizeof(double);
 }
 
 bool gram_fits(int s, int n_max, int r) { return n_max <= kGN && s <= 8 * kCh && s - n_max == r && r >= 1; }

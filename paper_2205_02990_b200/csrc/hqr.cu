@@ -1382,6 +1382,185 @@ HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* ou
 
 }  // namespace
 
+// Panel factorisation by CholeskyQR + Householder reconstruction (Ballard et
+// al.), for the fused kernel's panel group (NTG threads, named barrier 1).
+// The panel block P = A(j0:m, j0:j0+32) (rows below the finished R):
+//   Gp = P^T P = R^T R (tensor cores; Cholesky, row-owned, one warp),
+//   Q1 = P R^{-1} (tensor cores, in place),
+//   Q1(0:32, :) - S = L U with s_j = -sign of the current pivot (one warp),
+//   L2 = Q1(32:, :) U^{-1} (tensor cores, in place),
+//   T = -U S L^{-T}, R_hh = S R.
+// In exact arithmetic these are the reflectors (and T, R) the column-by-column
+// Householder chain (dlarfg signs) produces -- Householder QR is unique for a
+// given sign rule -- so the panel leaves A / T exactly as panel_factor_r +
+// form_t would, without a 32-step reduction chain.  Returns false (group-
+// uniform) for panels the chain must factor: partial panels, a Cholesky
+// breakdown, or min R_ii < 1e-2 max R_ii (the Gram squares the panel's
+// condition number; the chain also carries the reference's sigma screen).
+template <int NTG>
+__device__ __noinline__ bool panel_factor_gram(double* A, int lda, int m, int j0, int nbp, double* G, double* T,
+                                               double* scr, int* s_flag) {
+  if (nbp != kP) return false;
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mp = round_up(m, 8);
+  double* sg = scr;   // signs s_j
+  // 1. Gp = P^T P (32 x 32, row-major in G): 16 tiles of 8 x 8
+  for (int tile = warp; tile < 16; tile += nw) {
+    const int fi = tile >> 2, fj = tile & 3;
+    const double* ci = A + (j0 + 8 * fi + g) * lda + t;
+    const double* cj = A + (j0 + 8 * fj + g) * lda + t;
+    double c[4][2] = {};
+    for (int k = j0; k < mp; k += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + 4 * u < mp) dmma8x8x4(c[u][0], c[u][1], ci[k + 4 * u], cj[k + 4 * u]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + e] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
+  }
+  gsync<NTG>();
+  // 2. Cholesky (row i in lane i), R into G's upper triangle; R^{-1} into T
+  if (warp == 0) {
+    double c[kP];
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? G[lane * kLdT + k] : 0.0;
+    const double gmax = warp_max(G[lane * kLdT + lane]);
+    bool ok = gmax > 0.0 && gmax < 1e300;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const double d = __shfl_sync(0xffffffffu, c[j], j);
+      ok = ok && (d > 1e-4 * gmax);                  // R_jj >= 1e-2 max R_ii (approximately)
+      const double rs = rsqrt_nr(d);
+      if (lane == j) {
+#pragma unroll
+        for (int k = 0; k < kP; ++k)
+          if (k >= j) c[k] *= rs;
+      }
+      double rji = 0.0;
+#pragma unroll
+      for (int k = j + 1; k < kP; ++k) {
+        const double rk = __shfl_sync(0xffffffffu, c[k], j);
+        if (k == lane) rji = rk;
+        if (lane > j && k >= lane) c[k] = fma(-rji, rk, c[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+      if (k >= lane) G[lane * kLdT + k] = c[k];
+    __syncwarp();
+    // row lane of R^{-1}: x R = e_lane
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < kP; ++k) {
+      c[k] *= rcp_nr(G[k * kLdT + k]);
+#pragma unroll
+      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], G[k * kLdT + l], c[l]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) T[lane * kLdT + k] = c[k];
+    if (lane == 0) *s_flag = __all_sync(0xffffffffu, ok) ? 1 : 0;
+    else __all_sync(0xffffffffu, ok);
+  }
+  gsync<NTG>();
+  if (!*s_flag) return false;
+  // 3. Q1 = P R^{-1} in place, 8-row blocks per warp
+  for (int r0 = j0 + 8 * warp; r0 < mp; r0 += 8 * nw) {
+    double a[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
+    double acc[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
+  }
+  gsync<NTG>();
+  // 4. sign-chosen LU of the top 32 x 32 block (row lane in lane); U^{-1}
+  //    into T (R^{-1} is dead); R_hh = S R into A's upper triangle (U is dead
+  //    once U^{-1} and the T rows are formed); T = -U S L^{-T} rows into G
+  if (warp == 0) {
+    double c[kP];
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = A[(j0 + lane) + (j0 + k) * lda];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      double dinv = 0.0;
+      if (lane == j) {
+        const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
+        c[j] -= sj;
+        sg[j] = sj;
+        dinv = rcp_nr(c[j]);
+      }
+      dinv = __shfl_sync(0xffffffffu, dinv, j);
+      const double l = c[j] * dinv;
+      if (lane > j) c[j] = l;
+#pragma unroll
+      for (int k = j + 1; k < kP; ++k) {
+        const double uk = __shfl_sync(0xffffffffu, c[k], j);
+        if (lane > j) c[k] = fma(-l, uk, c[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) A[(j0 + lane) + (j0 + k) * lda] = c[k];
+    __syncwarp();
+    // column lane of U^{-1}: U z = e_lane, back substitution (c reused)
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = kP - 1; k >= 0; --k) {
+      c[k] *= rcp_nr(A[(j0 + k) + (j0 + k) * lda]);
+#pragma unroll
+      for (int q = 0; q < k; ++q) c[q] = fma(-A[(j0 + q) + (j0 + k) * lda], c[k], c[q]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) T[k * kLdT + lane] = c[k];
+    // T row lane: -(U S) then forward substitution with L (unit lower)
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? -A[(j0 + lane) + (j0 + k) * lda] * sg[k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+#pragma unroll
+      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], A[(j0 + l) + (j0 + k) * lda], c[l]);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+      if (k >= lane) A[(j0 + lane) + (j0 + k) * lda] = sg[lane] * G[lane * kLdT + k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kP; ++k) G[lane * kLdT + k] = c[k];
+  }
+  gsync<NTG>();
+  // 5. L2 = Q1(32:, :) U^{-1} in place
+  for (int r0 = j0 + kP + 8 * warp; r0 < mp; r0 += 8 * nw) {
+    double a[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
+    double acc[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
+  }
+  gsync<NTG>();
+  // 6. T from G
+  for (int e = ltid<NTG>(); e < kP * kP; e += gthreads<NTG>()) T[(e / kP) * kLdT + e % kP] = G[(e / kP) * kLdT + e % kP];
+  gsync<NTG>();
+  return true;
+}
+
 // TM: the box's Y rows live in tensor memory for the whole sweep (n_max <=
 // 128 rows -> TMEM lanes, s <= 256 fp64 columns), so the Y group's three
 // products per panel and the solve read and write Y there instead of
@@ -1423,6 +1602,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   double* T = Tscr + 384;
   double* A = T + round_up(kP * kLdT, 2);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_ready + 34);
+  int* s_pflag = reinterpret_cast<int*>(s_ready + 34) + 1;   // panel_factor_gram verdict
 
   // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1.
   // Each column is one contiguous Omega row: TMA bulk copies (one per column)
@@ -1526,6 +1706,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       if (lt == 0)
         for (int p = 0; p < npanel; ++p) mbar_arrive(&s_ready[p]);   // every panel (and T) is final
     }
+    int nhh = 0;   // panels factored by the Householder chain so far (barrier parity)
     for (int p = 0; p < (PRE ? 0 : npanel); ++p) {
       const int j0 = p * kP, nbp = min(kP, n - j0);
       if (p >= 2) mbar_wait(&s_ready[16 + p - 2], 0);   // panels <= p-2 applied to my columns by group Y
@@ -1537,10 +1718,20 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         gsync<256>();
       }
       if (lt == 0) FUSED_MARK(22 + 2 * p);
-      if constexpr (MR <= 6) panel_factor_r<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
-      else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(p & 1), G);
+#ifdef HBS_GRAM_PANEL   // experiment (measured slower: the single-warp 32-step factorisations)
+      const bool gp = panel_factor_gram<256>(A, lda, m, j0, nbp, G, T, Tscr, s_pflag);
+#else
+      const bool gp = false;
+      (void)s_pflag;
+#endif
+      if (!gp) {
+        // Householder chain; the step barriers complete once per chain-factored panel
+        if constexpr (MR <= 6) panel_factor_r<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
+        else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
+        ++nhh;
+      }
       if (lt == 0) FUSED_MARK(42 + p);
-      form_t<256>(T, Tscr, G, s_tau, j0, nbp);
+      if (!gp) form_t<256>(T, Tscr, G, s_tau, j0, nbp);
       for (int e = lt; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
       __threadfence_block();
       gsync<256>();

@@ -94,6 +94,21 @@ class CudaEngine:
         return a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
 
 
+def _all_gather_flat(out, inp, group):
+    """all_gather_into_tensor over NCCL; over other backends (gloo: the CPU
+    multi-process tests, or CUDA ranks without NCCL) the tensors are staged
+    through host memory."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return out
+    world = dist.get_world_size(group)
+    host = inp.detach().cpu().contiguous()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+    return out
+
+
 def _agree_on_failure(fail, group):
     """All ranks adopt the first failure in sweep order (deepest level,
     lowest node id) so they raise the same IllConditionedProbeError."""
@@ -136,7 +151,7 @@ def compress_distributed(local_samples, tree: ClusterTree, config: CompressionCo
     # one all-gather of the level-lg lifted halves: (world, 4, r, s)
     half = torch.stack([m.reshape(r, s) for m in local.top_quad]).contiguous().reshape(-1)
     gathered = torch.empty(world * half.numel(), dtype=half.dtype, device=half.device)
-    dist.all_gather_into_tensor(gathered, half, group=group)
+    _all_gather_flat(gathered, half, group)
     gathered = gathered.reshape(world, 4, r, s)
     top_quad = tuple(gathered[:, i].reshape(world * r, s).contiguous() for i in range(4))
     top = engine.run(tree, part.top_specs, top_quad, s, r, tol, with_root=True)
@@ -331,7 +346,7 @@ class DistributedOperator:
             return self.down_local(q, qhat, u1, transpose)
         lg = part.lg
         qtop = torch.empty(part.world * r * q.shape[1], dtype=torch.float64, device=self.device)
-        dist.all_gather_into_tensor(qtop, qhat[lg].reshape(-1), group=self.group)
+        _all_gather_flat(qtop, qhat[lg].reshape(-1), self.group)
         ulg = self.top(qtop.reshape(part.world * r, q.shape[1]), transpose)
         return self.down_local(q, qhat, ulg[part.rank * r:(part.rank + 1) * r], transpose)
 
@@ -363,7 +378,7 @@ class DistributedCompressor:
         w, r, s = self.part.world, self.part.r, self.s
         for i, m in enumerate(self.local.top_quad):
             self.half[i].copy_(m.reshape(r, s))
-        dist.all_gather_into_tensor(self.gathered, self.half.reshape(-1), group=self.group)
+        _all_gather_flat(self.gathered, self.half.reshape(-1), self.group)
         g = self.gathered.reshape(w, 4, r, s)
         for i in range(4):
             self.top_quad[i].copy_(g[:, i].reshape(w * r, s))

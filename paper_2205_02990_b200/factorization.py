@@ -173,28 +173,39 @@ class HbsFactorization:
 
     def validate(self):
         """Orthonormality of every basis and finiteness of all blocks
-        (factorization.py:69-86), evaluated on the device per level."""
+        (factorization.py:69-86), evaluated on the device per level; the first
+        failure is reported in the reference's order (level order; per node:
+        column basis, row basis, discrepancy)."""
         r = self.rank
         eye = torch.eye(r, dtype=torch.float64, device=self.device)
         for level in range(1, self.tree.depth + 1):
             g = self.geometry[level]
             u, v, d = self.levels[level]
             sizes = np.diff(g.begins_host)
-            for basis, kind in ((u, "column basis"), (v, "row basis")):
+            defects = []
+            for basis in (u, v):
                 if (sizes == sizes[0]).all():
                     blocks = basis.view(g.nbox, int(sizes[0]), r)
-                    defect = torch.linalg.matrix_norm(blocks.transpose(1, 2) @ blocks - eye)
+                    defects.append(torch.linalg.matrix_norm(blocks.transpose(1, 2) @ blocks - eye))
                 else:
-                    defect = torch.stack([torch.linalg.matrix_norm(
-                        basis[a - g.begins_host[0]:b - g.begins_host[0]].T @ basis[a - g.begins_host[0]:b - g.begins_host[0]] - eye)
-                        for a, b in zip(g.begins_host[:-1], g.begins_host[1:])])
-                bad = torch.nonzero(~(defect <= _ORTHONORMALITY_TOL))
-                if bad.numel():
-                    j = int(bad[0, 0])
-                    nid = (1 << level) - 1 + j
-                    raise ValueError(f"node {nid}: {kind} orthonormality defect {float(defect[j]):.3e}")
-            if not bool(torch.isfinite(d).all()):
-                raise ValueError(f"level {level}: discrepancy block has non-finite entries")
+                    b0 = g.begins_host[0]
+                    defects.append(torch.stack([torch.linalg.matrix_norm(basis[a - b0:b - b0].T @ basis[a - b0:b - b0] - eye)
+                                                for a, b in zip(g.begins_host[:-1], g.begins_host[1:])]))
+            bad_u, bad_v = (~(x <= _ORTHONORMALITY_TOL) for x in defects)
+            bad_d = torch.zeros(g.nbox, dtype=torch.bool, device=self.device)
+            nonfinite = torch.nonzero(~torch.isfinite(d)).reshape(-1)
+            if nonfinite.numel():
+                sq = torch.as_tensor(g.sq_host, device=self.device)
+                bad_d[torch.searchsorted(sq, nonfinite, right=True) - 1] = True
+            any_bad = bad_u | bad_v | bad_d
+            if bool(any_bad.any()):
+                j = int(torch.nonzero(any_bad)[0, 0])
+                nid = (1 << level) - 1 + j
+                if bool(bad_u[j]):
+                    raise ValueError(f"node {nid}: column basis orthonormality defect {float(defects[0][j]):.3e}")
+                if bool(bad_v[j]):
+                    raise ValueError(f"node {nid}: row basis orthonormality defect {float(defects[1][j]):.3e}")
+                raise ValueError(f"node {nid}: discrepancy block has non-finite entries")
         if not bool(torch.isfinite(self.root_device).all()):
             raise ValueError("root core has non-finite entries")
         return self

@@ -38,12 +38,14 @@ def dense_oracle(a, device=None) -> MatVecOracle:
         a_dev = torch.from_numpy(np.ascontiguousarray(a)).to(device or "cuda")
     if a_dev.ndim != 2 or a_dev.shape[0] != a_dev.shape[1]:
         raise DimensionError(f"dense oracle needs a square matrix, got shape {tuple(a_dev.shape)}")
-    return MatVecOracle(a_dev.shape[0], lambda x: dense_apply(a_dev, x), lambda x: dense_apply(a_dev, x, True))
+    return MatVecOracle(a_dev.shape[0], lambda x: dense_apply(a_dev, x), lambda x: dense_apply(a_dev, x, True),
+                        device_aware=True)
 
 
 def hbs_oracle(f: HbsFactorization) -> MatVecOracle:
     """Matrix-free oracle of a telescoping factorization (operators.py:221-228)."""
-    return MatVecOracle(f.n, lambda x: apply_matrix(f, x), lambda x: apply_matrix(f, x, transpose=True))
+    return MatVecOracle(f.n, lambda x: apply_matrix(f, x), lambda x: apply_matrix(f, x, transpose=True),
+                        device_aware=True)
 
 
 def log_kernel_matrix(n: int, device=None) -> torch.Tensor:

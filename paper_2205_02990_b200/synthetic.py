@@ -94,8 +94,6 @@ def _gen_level(gen, begins, k, leaf, decay, dev):
         d[:, k:, :k] = _coupling(gen, nbox, k, decay, dev)
         return u.contiguous(), v.contiguous(), d.reshape(-1).contiguous()
     us, vs, ds = [], [], []
-    for m in np.unique(sizes):
-        pass
     if (sizes == sizes[0]).all():
         m = int(sizes[0])
         u = _orthonormal(gen, nbox, m, k, dev).reshape(-1, k)

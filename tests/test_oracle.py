@@ -87,17 +87,15 @@ def test_gaussian_stream_frozen():
 
 
 def test_power_method_matches_reference_semantics(reference_hbs):
-    """verify.power_method_relnorm restates linalg.py:108-129 (same start stream)."""
-    torch = pytest.importorskip("torch")
+    """verify.power_method_relnorm restates linalg.py:108-129 (same start
+    stream) and, like the reference, hands plain callables 1-D numpy vectors."""
+    pytest.importorskip("torch")
     from paper_2205_02990_b200.verify import power_method_relnorm
     rng = np.random.default_rng(7)
     a = rng.standard_normal((32, 32))
-    op = lambda x: (torch.from_numpy(a) @ x) if isinstance(x, torch.Tensor) else a @ x
-    opt = lambda x: (torch.from_numpy(a).T @ x) if isinstance(x, torch.Tensor) else a.T @ x
     d = np.ones(32)
     d[0] = 3.0
-    ed = lambda x: torch.from_numpy(d).reshape(-1, 1) * x
-    mine = power_method_relnorm(ed, ed, op, opt, 32, iters=20, seed=4, device="cpu")
-    ref = reference_hbs.power_method_relnorm(lambda x: d * x, lambda x: d * x, lambda x: a @ x, lambda x: a.T @ x,
-                                             32, iters=20, seed=4)
+    ops = (lambda x: d * x, lambda x: d * x, lambda x: a @ x, lambda x: a.T @ x)
+    mine = power_method_relnorm(*ops, 32, iters=20, seed=4, device="cpu")
+    ref = reference_hbs.power_method_relnorm(*ops, 32, iters=20, seed=4)
     assert abs(mine - ref) <= 1e-12 * ref
