@@ -105,6 +105,19 @@ int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, 
                  double tol, const double* omega, double* vt, double* r, double* tau, double* t, double* rinv,
                  double* scratch, int32_t* status, void* stream);
 
+/* Building block: the same factorisation of Omega_tau^T by Gram / Cholesky and
+ * a sign-chosen LU that reconstructs the Householder form (gram.cu), for
+ * boxes with nullity s - rows == r.  Per box b (uniform stride rows x s):
+ *   fac  : row j = column j of [R (upper, on/above the diagonal) + V1 (below); V2],
+ *          i.e. hbs_probe_qr's r and vt in one array
+ *   t    : ceil(rows/32) compact-WY T blocks (32 x 32, row-major)
+ *   flag[b] = 1 when the box needs the Householder kernel instead (shape,
+ *          Cholesky breakdown or min R_ii < 1e-3 max R_ii); status[b] = 0
+ *          otherwise.  Needs max_rows <= 128, s <= 256. */
+int hbs_gram_probe_factor(int64_t nbox, const int64_t* row_begin, int max_rows, int s, int r,
+                          const double* omega, double* fac, double* t, int32_t* flag, int32_t* status,
+                          void* stream);
+
 /* Building block: batched reduced Householder QR with explicit Q -- the
  * reference's col() (linalg.py:35-49: np.linalg.qr(b)[0][:, :r]) for every
  * box of a level.  b and q are packed (rows x r) row-major with box b at row

@@ -39,6 +39,7 @@ SIGNATURES = {
     "hbs_probe_qr_scratch_bytes": ([_I64, _I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_basis_qr_scratch_bytes": ([_I64, _I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_basis_qr": ([_I64, _P, _P, _I, _I, _P, _P, _P, _P], _I),
+    "hbs_gram_probe_factor": ([_I64, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P], _I),
     "hbs_basis_orth": ([_I64, _P, _P, _I, _I, _P, _P, _P, _P, _P], _I),
     "hbs_probe_qr": ([_I64, _P, _P, _I, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "hbs_root_workspace_bytes": ([_I, _I, ctypes.POINTER(_SZ)], _I),

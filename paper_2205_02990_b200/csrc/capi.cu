@@ -384,6 +384,23 @@ int hbs_probe_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, 
   return launch_hqr(g, 1, static_cast<cudaStream_t>(stream));
 }
 
+int hbs_gram_probe_factor(int64_t nbox, const int64_t* row_begin, int max_rows, int s, int r,
+                          const double* omega, double* fac, double* t, int32_t* flag, int32_t* status,
+                          void* stream) {
+  if (nbox < 1 || max_rows < 1 || s < max_rows || !flag) return HBS_ERR_DIMENSION;
+  if (!gram_fits(s, max_rows, r)) return HBS_ERR_UNSUPPORTED;
+  GramArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  ga.geo = LevelGeo{row_begin, nullptr, nbox};
+  ga.s = s; ga.r = r; ga.flag = flag;
+  GramSide& G = ga.side[0];
+  G.om = omega; G.om_c_rb = s;
+  G.fac = fac; G.fac_stride = (int64_t)max_rows * s;
+  G.t = t; G.t_stride = (int64_t)((max_rows + kNB - 1) / kNB) * kNB * kNB;
+  G.status = status;
+  return launch_gram(ga, 1, static_cast<cudaStream_t>(stream));
+}
+
 int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,
                  const double* b, double* q, double* scratch, void* stream) {
   if (nbox < 1 || max_rows < r || r < 1) return HBS_ERR_DIMENSION;

@@ -66,92 +66,97 @@ struct GR {
   HBS_DEV double& at(int i, int j) const { return blk(i >> 4, j >> 4)[bsw(i & 15, j & 15)]; }
 };
 
+// 1/sqrt(a) and 1/a from float seeds and two Newton steps in double, with
+// exact power-of-two range reduction instead of the library slow paths (whose
+// subroutine calls would push the callers' register arrays to local memory).
 HBS_DEV double rsqrt_g(double a) {
-  if (!(a > 1e-30 && a < 1e30)) return rsqrt(a);
+  double sc = 1.0;
+  // (one exact power-of-two step covers 1e-60 .. 1e60 -- far beyond any
+  // Gram entry that passes the screens)
+  if (a > 1e30) { a *= 0x1p-100; sc = 0x1p-50; }
+  if (a < 1e-30 && a > 0.0) { a *= 0x1p100; sc = 0x1p50; }
   double y = static_cast<double>(rsqrtf(static_cast<float>(a)));
   const double ha = 0.5 * a;
   y = y * fma(-ha * y, y, 1.5);
   y = y * fma(-ha * y, y, 1.5);
-  return y;
+  return y * sc;
 }
 HBS_DEV double rcp_g(double a) {
-  const double m = fabs(a);
-  if (!(m > 1e-30 && m < 1e30)) return 1.0 / a;
-  double y = static_cast<double>(__frcp_rn(static_cast<float>(a)));
+  double sc = 1.0;
+  if (fabs(a) > 1e30) { a *= 0x1p-100; sc = 0x1p-100; }
+  if (fabs(a) < 1e-30 && a != 0.0) { a *= 0x1p100; sc = 0x1p100; }
+  float yf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(static_cast<float>(a)));   // (rcp.rn has a slow-path call)
+  double y = static_cast<double>(yf);
   y = fma(y, fma(-a, y, 1.0), y);
   y = fma(y, fma(-a, y, 1.0), y);
-  return y;
+  y = fma(y, fma(-a, y, 1.0), y);
+  return y * sc;
 }
 
 // Cholesky of the diagonal block Bd (upper triangle = current Schur
-// complement) in place, row-owned: lane i (and its mirror i + 16) holds row i
-// in registers and row j of R is broadcast by shuffles.  rd[j] = R_jj.  Then
-// Ri = R_oo^{-1} (upper; swizzled block).  One warp; false on breakdown.
-HBS_DEV bool chol16_inv(double* Bd, double* rd, double* Ri, double floor_) {
-  const int lane = threadIdx.x & 31, i = lane & 15;
+// complement) in place.  Column-owned: lane k (and its mirror k + 16) holds
+// column k; row j of R is broadcast through `row` (16 doubles of shared
+// memory).  ri[j] = 1 / R_jj.  One warp; false on breakdown.
+HBS_DEV bool chol16(double* Bd, double* ri, double* row, double floor_) {
+  const int lane = threadIdx.x & 31, kc = lane & 15;
   double c[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) c[k] = (k >= i) ? Bd[bsw(i, k)] : 0.0;
+  for (int i = 0; i < 16; ++i) c[i] = Bd[bsw(i, kc)];   // rows > kc are don't-care (masked below)
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const double d = __shfl_sync(0xffffffffu, c[j], j);
     ok = ok && (d > floor_) && (d < 1e300);
     const double rs = rsqrt_g(d);
-    if (i == j) {
+    c[j] = (kc == j) ? d * rs : (kc > j ? c[j] * rs : 0.0);
+    if (lane == j) ri[j] = rs;
+    row[kc] = c[j];
+    __syncwarp();
+    const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k >= j) c[k] *= rs;
+    for (int h = 0; h < 8; ++h) {
+      if (2 * h + 1 > j) {
+        const double2 v = r2[h];
+        if (2 * h > j) c[2 * h] = (2 * h <= kc) ? fma(-v.x, c[j], c[2 * h]) : c[2 * h];
+        c[2 * h + 1] = (2 * h + 1 <= kc) ? fma(-v.y, c[j], c[2 * h + 1]) : c[2 * h + 1];
+      }
     }
-    double rj[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k >= j) rj[k] = __shfl_sync(0xffffffffu, c[k], j);
-    double rji = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k > j && k == i) rji = rj[k];
-    if (i > j) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k > j && k >= i) c[k] = fma(-rji, rj[k], c[k]);
-    }
+    __syncwarp();
   }
   if (lane < 16) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k >= i) Bd[bsw(i, k)] = c[k];
-    double di = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k == i) di = c[k];
-    rd[i] = di;
+    for (int i = 0; i < 16; ++i)
+      if (i <= kc) Bd[bsw(i, kc)] = c[i];
   }
-  __syncwarp();
-  // row i of R^{-1}: x R = e_i (forward over columns, right-looking)
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Ri = R^{-1} (upper) of a finished diagonal block; lane i < 16: row i
+// (x R = e_i, right-looking over columns); ri = 1 / R_jj.
+HBS_DEV void rinv16(const double* Bd, const double* ri, double* Ri) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
   double x[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) x[k] = (k == i) ? 1.0 : 0.0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    x[k] *= rcp_g(Bd[bsw(k, k)]);
+    x[k] *= ri[k];
 #pragma unroll
-    for (int l = 0; l < 16; ++l)
-      if (l > k) x[l] = fma(-x[k], Bd[bsw(k, l)], x[l]);
+    for (int l = k + 1; l < 16; ++l) x[l] = fma(-x[k], Bd[bsw(k, l)], x[l]);
   }
   if (lane < 16) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) Ri[bsw(i, k)] = x[k];
   }
-  return __all_sync(0xffffffffu, ok);
 }
 
 // LU of the 16 x 16 diagonal block of M at (ko, ko) with the Householder sign
 // rule, row-owned: pivot row j first loses s_j R(ko + j, ko + j:) with s_j =
 // -sign of its current diagonal (|pivot| = |a| + R_jj), then is broadcast by
 // shuffles.  Unit lower L below, U' on / above the diagonal (in X);
-// sg[j] = s_j; Li = L^{-1} (unit lower) and Ui = U'^{-1} (upper), swizzled.
-HBS_DEV void lu16_inv(double* X, int ko, const double* Rd, double* sg, double* Li, double* Ui) {
+// sg[j] = s_j.
+HBS_DEV void lu16(double* X, int ko, const double* Rd, double* sg) {
   const int lane = threadIdx.x & 31, i = lane & 15;
   double c[16], rr[16];
 #pragma unroll
@@ -159,62 +164,68 @@ HBS_DEV void lu16_inv(double* X, int ko, const double* Rd, double* sg, double* L
     c[k] = X[(ko + i) + (ko + k) * kLdX];
     rr[k] = (k >= i) ? Rd[bsw(i, k)] : 0.0;
   }
-#pragma unroll
+#pragma unroll 16
   for (int j = 0; j < 16; ++j) {
-    double dinv = 0.0;
-    if (i == j) {
-      const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
+    // pivot row j (lane j) loses s_j R(j, j:) (branch-free: keeps c[] in registers)
+    const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
+    const double sm = (i == j) ? -sj : 0.0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k >= j) c[k] = fma(-sj, rr[k], c[k]);
-      dinv = rcp_g(c[j]);
-      if (lane == j) sg[j] = sj;
-    }
-    dinv = __shfl_sync(0xffffffffu, dinv, j);
-    double uj[16];
+    for (int k = j; k < 16; ++k) c[k] = fma(sm, rr[k], c[k]);
+    if (lane == j) sg[j] = sj;
+    const double dinv = __shfl_sync(0xffffffffu, rcp_g(c[j]), j);
+    const double l = (i > j) ? c[j] * dinv : 0.0;
+    if (i > j) c[j] = l;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k > j) uj[k] = __shfl_sync(0xffffffffu, c[k], j);
-    if (i > j) {
-      const double l = c[j] * dinv;
-      c[j] = l;
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k > j) c[k] = fma(-l, uj[k], c[k]);
+    for (int k = j + 1; k < 16; ++k) {
+      const double uk = __shfl_sync(0xffffffffu, c[k], j);
+      c[k] = fma(-l, uk, c[k]);
     }
   }
   if (lane < 16) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) X[(ko + i) + (ko + k) * kLdX] = c[k];
   }
-  __syncwarp();
-  // lanes 0..15: column i of L^{-1} (unit lower); lanes 16..31: column i of U'^{-1}
+}
+
+// Li = L^{-1} (unit lower): lane i < 16 computes column i.
+HBS_DEV void linv16(const double* X, int ko, double* Li) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
   double z[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+#pragma unroll
+    for (int q = m + 1; q < 16; ++q)
+      if (m >= i) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
   if (lane < 16) {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
-#pragma unroll
-    for (int m = 0; m < 16; ++m)
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (q > m && m >= i) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
-#pragma unroll
     for (int m = 0; m < 16; ++m) Li[bsw(m, i)] = z[m];
-  } else {
+  }
+}
+
+// Ui = U'^{-1} (upper): lane i < 16 computes column i (back substitution).
+HBS_DEV void uinv16(const double* X, int ko, double* Ui) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  double z[16];
 #pragma unroll
-    for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
+  for (int m = 0; m < 16; ++m) z[m] = (m == i) ? 1.0 : 0.0;
 #pragma unroll
-    for (int m = 15; m >= 0; --m) {
-      if (m <= i) {
-        z[m] *= rcp_g(X[(ko + m) + (ko + m) * kLdX]);
+  for (int m = 15; m >= 0; --m) {
+    if (m <= i) {
+      z[m] *= rcp_g(X[(ko + m) + (ko + m) * kLdX]);
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q < m) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
-      }
+      for (int q = 0; q < m; ++q) z[q] = fma(-X[(ko + q) + (ko + m) * kLdX], z[m], z[q]);
     }
+  }
+  if (lane < 16) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) Ui[bsw(m, i)] = z[m];
   }
+}
+
+HBS_DEV void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace
@@ -238,9 +249,9 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
   double* Uinv = Yr + 2 * kGN * kLdC;                // inverses of U' diagonal blocks (V2)
   double* Rinv = Uinv + 8 * kBlk;                    // R_oo^{-1} of the current Cholesky block
   double* Linv = Rinv + kBlk;                        // L_oo^{-1} of the current LU block
-  double* rdiag = Linv + kBlk;                       // R_jj
-  double* sg = rdiag + kGN;                          // Householder signs s_j
-  int* s_ok = reinterpret_cast<int*>(sg + kGN);
+  double* sg = Linv + kBlk;                          // Householder signs s_j
+  double* rinvd = sg + kGN;                          // 1 / R_jj
+  int* s_ok = reinterpret_cast<int*>(rinvd + kGN);
   const GR Gm{Yr, nb};
 
   const double* om = S.om + S.om_c_rb * args.geo.row_begin[b];
@@ -332,13 +343,22 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
   const double floor_ = 1e-24 * gmax;
   for (int it = 0; it <= nb; ++it) {
     const int oc = it, ol = it - 1, kl = 16 * ol;
-    if (warp == 0 && oc < nb) {
-      const bool ok = chol16_inv(Gm.blk(oc, oc), rdiag + 16 * oc, Rinv, floor_);
-      if (lane == 0) *s_ok = ok;
-    } else if (warp == 1 && ol >= 0) {
-      lu16_inv(X, kl, Gm.blk(ol, ol), sg + kl, Linv, Uinv + ol * kBlk);
+    // warps 0 / 3: Cholesky, then R_oo^{-1}; warps 1 / 2 / 4: LU, then L^{-1} and U'^{-1}
+    if (oc < nb && (warp == 0 || warp == 3)) {
+      if (warp == 0) {
+        const bool ok = chol16(Gm.blk(oc, oc), rinvd + 16 * oc, Rinv, floor_);   // (Rinv: row buffer until warp 3 fills it)
+        if (lane == 0) *s_ok = ok;
+      }
+      named_sync(1, 64);
+      if (warp == 3) rinv16(Gm.blk(oc, oc), rinvd + 16 * oc, Rinv);
+    } else if (ol >= 0 && (warp == 1 || warp == 2 || warp == 4)) {
+      if (warp == 1) lu16(X, kl, Gm.blk(ol, ol), sg + kl);
+      named_sync(2, 96);
+      if (warp == 2) linv16(X, kl, Linv);
+      if (warp == 4) uinv16(X, kl, Uinv + ol * kBlk);
     }
     __syncthreads();
+    if (it == 2) GR_MARK(5);
     if (!*s_ok) {
       if (threadIdx.x == 0) *myflag = 1;
       return;
@@ -398,47 +418,81 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
       }
     }
     __syncthreads();
-    // (C) trailing updates, 8 x 8 tiles: Cholesky (upper block triangle) then LU (square)
+    if (it == 2) GR_MARK(6);
+    // (C) trailing updates in 16 x 16 units (four independent accumulator
+    // chains): Cholesky (upper block triangle) then LU (square)
     const int mb = nbc;
-    const int uc = mb * (mb + 1) / 2 * 4;
-    const int mt = 2 * nbl;
-    const int ut = uc + mt * mt;
+    const int uc = mb * (mb + 1) / 2;
+    const int ut = uc + nbl * nbl;
     for (int u = warp; u < ut; u += kGT / 32) {
       if (u < uc) {
-        int q = u >> 2, bi = 0;
+        int q = u, bi = 0;
         while (q >= mb - bi) { q -= mb - bi; ++bi; }
         const int bj = bi + q + oc + 1;
         bi += oc + 1;
-        const int fi = (u >> 1) & 1, fj = u & 1;
-        if (bi == bj && fi > fj) continue;
         const double* ra = Gm.blk(oc, bi);
         const double* rb2 = Gm.blk(oc, bj);
         double* cb = Gm.blk(bi, bj);
-        double c0 = cb[bsw(8 * fi + g, 8 * fj + 2 * t)], c1 = cb[bsw(8 * fi + g, 8 * fj + 2 * t + 1)];
+        double c[2][2][2];
 #pragma unroll
-        for (int k = 0; k < 16; k += 4)
-          dmma8x8x4(c0, c1, -ra[bsw(k + t, 8 * fi + g)], rb2[bsw(k + t, 8 * fj + g)]);
-        cb[bsw(8 * fi + g, 8 * fj + 2 * t)] = c0;
-        cb[bsw(8 * fi + g, 8 * fj + 2 * t + 1)] = c1;
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int fj = 0; fj < 2; ++fj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) c[fi][fj][e] = cb[bsw(8 * fi + g, 8 * fj + 2 * t + e)];
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          const double a0 = -ra[bsw(k + t, g)], a1 = -ra[bsw(k + t, 8 + g)];
+          const double b0 = rb2[bsw(k + t, g)], b1 = rb2[bsw(k + t, 8 + g)];
+          dmma8x8x4(c[0][0][0], c[0][0][1], a0, b0);
+          dmma8x8x4(c[0][1][0], c[0][1][1], a0, b1);
+          dmma8x8x4(c[1][0][0], c[1][0][1], a1, b0);
+          dmma8x8x4(c[1][1][0], c[1][1][1], a1, b1);
+        }
+#pragma unroll
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int fj = 0; fj < 2; ++fj) {
+            if (bi == bj && fi > fj) continue;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) cb[bsw(8 * fi + g, 8 * fj + 2 * t + e)] = c[fi][fj][e];
+          }
       } else {
         const int v = u - uc;
-        const int c0r = kl + 16 + 8 * (v / mt), d0 = kl + 16 + 8 * (v % mt);
-        double* cp = X + (c0r + g) + (d0 + 2 * t) * kLdX;
-        double c0 = cp[0], c1 = cp[kLdX];
+        const int c0r = kl + 16 + 16 * (v / nbl), d0 = kl + 16 + 16 * (v % nbl);
+        double c[2][2][2];
 #pragma unroll
-        for (int k = 0; k < 16; k += 4)
-          dmma8x8x4(c0, c1, -X[(c0r + g) + (kl + k + t) * kLdX], X[(kl + k + t) + (d0 + g) * kLdX]);
-        cp[0] = c0;
-        cp[kLdX] = c1;
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int fj = 0; fj < 2; ++fj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) c[fi][fj][e] = X[(c0r + 8 * fi + g) + (d0 + 8 * fj + 2 * t + e) * kLdX];
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          const double a0 = -X[(c0r + g) + (kl + k + t) * kLdX], a1 = -X[(c0r + 8 + g) + (kl + k + t) * kLdX];
+          const double b0 = X[(kl + k + t) + (d0 + g) * kLdX], b1 = X[(kl + k + t) + (d0 + 8 + g) * kLdX];
+          dmma8x8x4(c[0][0][0], c[0][0][1], a0, b0);
+          dmma8x8x4(c[0][1][0], c[0][1][1], a0, b1);
+          dmma8x8x4(c[1][0][0], c[1][0][1], a1, b0);
+          dmma8x8x4(c[1][1][0], c[1][1][1], a1, b1);
+        }
+#pragma unroll
+        for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+          for (int fj = 0; fj < 2; ++fj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) X[(c0r + 8 * fi + g) + (d0 + 8 * fj + 2 * t + e) * kLdX] = c[fi][fj][e];
       }
     }
     __syncthreads();
+    if (it == 2) GR_MARK(7);
+    if (it == 1) GR_MARK(8);
     if (it == nb - 1) GR_MARK(2);
   }
   // screen: the Gram squares cond(Omega); route doubtful boxes to Householder
   if (warp == 0) {
     double lo = INFINITY, hi = 0.0;
-    for (int j = lane; j < n; j += 32) { lo = fmin(lo, rdiag[j]); hi = fmax(hi, rdiag[j]); }
+    for (int j = lane; j < n; j += 32) { const double d = Gm.at(j, j); lo = fmin(lo, d); hi = fmax(hi, d); }
     lo = warp_min(lo);
     hi = warp_max(hi);
     if (lane == 0) *s_ok = (hi > 0.0) && isfinite(hi) && lo >= kFallbackRatio * hi;
@@ -510,28 +564,30 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
     if (j0 < n) {
       const int nbp = min(32, n - j0), i = lane;
       const int bo = j0 >> 4;
-      const double* Rb[2][2] = {{Gm.blk(bo, bo), Gm.blk(bo, min(bo + 1, nb - 1))},
-                                {Gm.blk(min(bo + 1, nb - 1), min(bo + 1, nb - 1)), nullptr}};
+      const int bo1 = min(bo + 1, nb - 1);
+      const double* Raa = Gm.blk(bo, bo);
+      const double* Rab = Gm.blk(bo, bo1);
+      const double* Rbb = Gm.blk(bo1, bo1);
       double z[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) z[j] = (j >= i && j < nbp && i < nbp) ? X[(j0 + i) + (j0 + j) * kLdX] : 0.0;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (k < nbp) {
-          const double* rk = Rb[k >> 4][0];
-          z[k] *= rcp_g(rk[bsw(k & 15, k & 15)]);
+          z[k] *= rinvd[j0 + k];
 #pragma unroll
           for (int l = 0; l < 32; ++l)
             if (l > k && l < nbp) {
-              const double* rbl = (k >> 4) == (l >> 4) ? Rb[k >> 4][0] : Rb[0][1];
+              const double* rbl = (k >> 4) ? Rbb : ((l >> 4) ? Rab : Raa);
               z[l] = fma(-z[k], rbl[bsw(k & 15, l & 15)], z[l]);
             }
         }
       }
 #pragma unroll
+      for (int k = 0; k < 32; ++k) z[k] = (k < nbp) ? z[k] * sg[j0 + k] : 0.0;
+#pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (k < nbp) {
-          z[k] *= sg[j0 + k];
 #pragma unroll
           for (int l = 0; l < 32; ++l)
             if (l > k && l < nbp) z[l] = fma(-z[k], X[(j0 + l) + (j0 + k) * kLdX], z[l]);
@@ -542,11 +598,14 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
       for (int j = 0; j < 32; ++j) tp[j] = -z[j];
     }
   }
+  GR_MARK(9);
   // ------------------------------------------------------------ R_hh and V1 rows
-  for (int e = threadIdx.x; e < n * n; e += kGT) {
-    const int j = e / n, i = e - j * n;
-    const double v = (i <= j) ? sg[i] * Gm.at(i, j) : X[i + j * kLdX];
-    fac[(size_t)j * s + i] = v;
+  // fac row j (column j of the A layout), one warp per row: R_hh above and on
+  // the diagonal, V1 below
+  for (int j = warp; j < n; j += kGT / 32) {
+    double* fr = fac + (size_t)j * s;
+    const double* xr = X + j * kLdX;
+    for (int i = lane; i < n; i += 32) fr[i] = (i <= j) ? sg[i] * Gm.at(i, j) : xr[i];
   }
   if (threadIdx.x == 0) {
     *myflag = 0;

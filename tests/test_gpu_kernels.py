@@ -187,3 +187,44 @@ def test_basis_orth_uneven_rows():
     for b, q in zip(blocks, qs):
         assert np.linalg.norm(q.T @ q - np.eye(24)) <= 1e-13 * 24
         assert np.linalg.norm(b - q @ (q.T @ b)) <= 1e-13 * np.linalg.norm(b)
+
+
+def gram_factor(blocks, s, r):
+    """hbs_gram_probe_factor on equal-size (rows x s) probe blocks."""
+    rows = blocks[0].shape[0]
+    nbox = len(blocks)
+    dev = torch.device("cuda")
+    om = torch.from_numpy(np.concatenate(blocks)).to(dev)
+    rb = torch.arange(nbox + 1, dtype=torch.int64, device=dev) * rows
+    npan = (rows + 31) // 32
+    fac = torch.zeros(nbox, rows, s, dtype=torch.float64, device=dev)
+    t = torch.zeros(nbox, npan, 32, 32, dtype=torch.float64, device=dev)
+    flag = torch.full((nbox,), -1, dtype=torch.int32, device=dev)
+    st = torch.full((nbox,), -1, dtype=torch.int32, device=dev)
+    _native.check(_native.lib().hbs_gram_probe_factor(nbox, rb.data_ptr(), rows, s, r, om.data_ptr(), fac.data_ptr(),
+                                                      t.data_ptr(), flag.data_ptr(), st.data_ptr(),
+                                                      torch.cuda.current_stream().cuda_stream), "gram")
+    torch.cuda.synchronize()
+    return fac.cpu().numpy(), t.cpu().numpy(), flag.cpu().numpy(), st.cpu().numpy()
+
+
+@pytest.mark.parametrize("rows,s", [(128, 192), (64, 96), (32, 48), (80, 120), (16, 40)])
+def test_gram_factor_reproduces_householder(rows, s):
+    """The Gram / Householder-reconstruction factorisation (gram.cu) yields the
+    LAPACK Householder reflectors, R and panel T of Omega^T up to rounding
+    (Householder QR is unique for dlarfg's sign rule)."""
+    rng = np.random.default_rng(rows + s)
+    r = s - rows
+    blocks = [rng.standard_normal((rows, s)) for _ in range(3)]
+    fac, t, flag, st = gram_factor(blocks, s, r)
+    assert not flag.any() and not st.any()
+    vt, rr, tau, tt, _, _ = probe_qr(blocks, s)
+    for b in range(3):
+        R = np.triu(fac[b][:, :rows].T)            # fac row j = column j of [R + V1; V2]
+        assert np.abs(R - rr[b]).max() <= 1e-11 * np.abs(rr[b]).max()
+        V = np.tril(fac[b].T, -1)[:, :rows] + np.eye(s, rows)
+        Vref = vt[b].T
+        assert np.abs(V - Vref).max() <= 1e-10
+        for p in range((rows + 31) // 32):
+            nbp = min(32, rows - 32 * p)
+            assert np.abs(t[b][p][:nbp, :nbp] - tt[b][p][:nbp, :nbp]).max() <= 1e-10

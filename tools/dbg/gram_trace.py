@@ -23,3 +23,6 @@ names = ["G", "Chol+LU to it=nb-1", "last LU it+screen", "V2/T/fac"]
 print("root-level CTA (runs alone): total %d cycles" % t[4])
 for i in range(4):
     print(f"  {names[i]:10s} {t[i + 1] - t[i]:8d} cycles")
+it1_end, a, b_, c_ = buf[8], buf[5], buf[6], buf[7]
+print(f"  iteration 2: A (diag chol/LU + inverses) {a - it1_end}  B (panels) {b_ - a}  C (trailing) {c_ - b_}")
+print(f"  tail: V2/T {buf[9] - buf[3]}  R_hh/V1 rows {buf[4] - buf[9]}")
