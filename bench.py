@@ -34,12 +34,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (N, k, leaf, s, r, decay)
+    # name: (N, k, leaf, s, r, decay); c3 is the ellipse log kernel (k = target rank)
     "c1": (4096, 16, 32, 48, 16, None),
     "c2": (1 << 16, 32, 64, 96, 32, None),
+    "c3": (1 << 15, 40, 80, 120, 40, None),
     "c4": (1 << 20, 64, 128, 192, 64, 0.9),
     "c5": (1 << 22, 128, 256, 384, 128, None),
 }
+KERNEL_CONFIGS = ("c3",)
 METRIC = "HBS compress-from-samples rows/s (fp64) at N=2^20,k=64"
 from paper_2205_02990_b200.roofline import PHASES, canonical_phase_flops, canonical_total_flops  # noqa: E402
 
@@ -124,12 +126,26 @@ class ReferenceSample:
     N-independent at fixed shape) and its seeded
     samples, drawn through the reference's own draw_samples / hbs_oracle."""
 
-    def __init__(self, cfg, n_sample):
+    def __init__(self, cfg, n_sample, kernel=False):
         from oracle import hbs_oracle as O
         _, k, leaf, s, r, decay = cfg
         self.n, self.r = n_sample, r
-        self.truth = O.baseline_generator(n_sample, leaf, k, seed=0, decay=decay)
         self.hbs = reference_module()
+        if kernel:   # config 3: dense ellipse log kernel through the dense oracle
+            a = O.ellipse_log_kernel(n_sample)
+            if self.hbs is not None:
+                from hbs import operators
+                self.tree = self.hbs.build_tree(n_sample, leaf)
+                self.samples = self.hbs.draw_samples(operators.dense_oracle(a), s, 0)
+                self.config = self.hbs.CompressionConfig(rank=r, leaf_threshold=leaf, probes=s)
+                self.kind = "reference"
+            else:
+                self.quad = O.samples_from(a, s, 0)
+                self.bounds = O.level_bounds(n_sample, O.tree_depth(n_sample, leaf))
+                self.kind = "port"
+            return
+        self.truth = O.baseline_generator(n_sample, leaf, k, seed=0, decay=decay)
+        self.bounds = self.truth.bounds
         if self.hbs is not None:
             from hbs import operators
             f = self.truth
@@ -154,7 +170,7 @@ class ReferenceSample:
             self.hbs.compress_from_samples(self.samples, self.tree, self.config)
         else:
             from oracle import hbs_oracle as O
-            O.compress(*self.quad, self.truth.bounds, self.r)
+            O.compress(*self.quad, self.bounds, self.r)
         return time.perf_counter() - t0
 
     def describe(self, cores):
@@ -171,7 +187,7 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    smp = ReferenceSample(cfg, min(args.ref_sample, cfg[0]))
+    smp = ReferenceSample(cfg, min(args.ref_sample, cfg[0]), kernel=args.config in KERNEL_CONFIGS)
     for _ in range(args.warmup):
         smp.step()
     times = [smp.step() for _ in range(args.steps)]
@@ -193,7 +209,7 @@ def cpu_baseline_leg(args, cfg):
     """The reference CPU path on a bounded sample (rank 0, N = 1): best of 3."""
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    smp = ReferenceSample(cfg, min(args.cpu_sample, cfg[0]))
+    smp = ReferenceSample(cfg, min(args.cpu_sample, cfg[0]), kernel=args.config in KERNEL_CONFIGS)
     times = [smp.step() for _ in range(3)]
     return {"value": smp.n / min(times), "unit": "rows/s", "cores": cores, "kind": smp.kind,
             "sample": smp.describe(cores) + f"; best of 3, {time.perf_counter() - t0:.1f} s incl. input generation"}
@@ -272,9 +288,33 @@ def run_distributed(args, cfg, world, rank, dev):
     dist.destroy_process_group()
 
 
+def make_workload(name, cfg, tree, dev, seed):
+    """Device-resident samples of a BASELINE config and the true operator's
+    apply: the section-8(d) HBS operator on torch's Philox stream (configs
+    1, 2, 4, 5; HBS sampler), or the ellipse log kernel (config 3; dense
+    DMMA sampler)."""
+    import torch
+    import paper_2205_02990_b200 as hb
+    from paper_2205_02990_b200 import operators, synthetic
+    N, k, leaf, s, r, decay = cfg
+    if name in KERNEL_CONFIGS:
+        a = hb.log_kernel_matrix(N, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        om = torch.randn(N, s, generator=g, dtype=torch.float64, device=dev)
+        ps = torch.randn(N, s, generator=g, dtype=torch.float64, device=dev)
+        y, z = operators.dense_apply(a, om), operators.dense_apply(a, ps, transpose=True)
+        return om, ps, y, z, lambda x: operators.dense_apply(a, x)
+    gen = synthetic.device_generator(tree, k, seed=seed, decay=decay, device=dev)
+    om, ps, y, z = synthetic.device_samples(gen, s, seed=seed)
+    return om, ps, y, z, lambda x: hb.apply_matrix(gen, x)
+
+
 def config_block(args, cfg, world):
     N, k, leaf, s, r, decay = cfg
-    return {"workload": f"{args.config}: exact-rank synthetic HBS, N={N} per GPU, k={k}, r={r}, leaf={leaf}, "
+    what = ("ellipse log kernel (numerical rank), dense DMMA sampler" if args.config in KERNEL_CONFIGS
+            else "exact-rank synthetic HBS, HBS sampler")
+    return {"workload": f"{args.config}: {what}, N={N} per GPU, k={k}, r={r}, leaf={leaf}, "
                         f"s={s}" + (f", coupling decay {decay}" if decay else ""),
             "N_per_gpu": N, "k": k, "r": r, "leaf": leaf, "s": s, "global_rows": N * world,
             "parallelism": f"subtree x{world}" if world > 1 else "single GPU",
@@ -324,9 +364,16 @@ def main():
         return
     tree = hb.build_tree(N, leaf)
     t0 = time.perf_counter()
-    gen = synthetic.device_generator(tree, k, seed=rank, decay=decay, device=dev)
-    om, ps, y, z = synthetic.device_samples(gen, s, seed=rank)
+    om, ps, y, z, apply_true = make_workload(args.config, cfg, tree, dev, rank)
+    # accuracy probe x = N(0,1) N x 8 and the true operator's A x, taken now so
+    # the generator's memory is released before the sweep's buffers (config 5)
+    xg = torch.Generator(device=dev)
+    xg.manual_seed(4)
+    x = torch.randn(N, 8, generator=xg, dtype=torch.float64, device=dev)
+    ax_true = apply_true(x)
+    del apply_true
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     t_gen = time.perf_counter() - t0
     plan = hb.CompressPlan(tree, s, r, device=dev)
     lib = hb._native.lib()
@@ -352,35 +399,21 @@ def main():
     value = N * world / (ms_step / 1e3)
 
     # accuracy of this run vs the true operator (probe x, 8 columns)
-    xg = torch.Generator(device=dev)
-    xg.manual_seed(4)
-    x = torch.randn(N, 8, generator=xg, dtype=torch.float64, device=dev)
     f = plan.factorization()
-    err = float(torch.linalg.norm(hb.apply_matrix(f, x) - hb.apply_matrix(gen, x)) /
-                torch.linalg.norm(hb.apply_matrix(gen, x)))
+    err = float(torch.linalg.norm(hb.apply_matrix(f, x) - ax_true) / torch.linalg.norm(ax_true))
 
     # roofline: live per-phase CUDA-event timing of one extra sweep
     peak_tf, peak_src = fp64_peak()
     phase_ms = {p: 0.0 for p in PHASES}
     phase_flops = {p: 0.0 for p in PHASES}
-    import ctypes
-    buf = (ctypes.c_float * 6)()
     quad = (om, ps, y, z)
     for idx, level in enumerate(range(tree.depth, 0, -1)):
         g = plan.geometry[level]
-        u, v, d = plan.levels[level]
-        out = plan.lift[idx % 2]
-        rc = lib.hbs_compress_level_profiled(
-            g.nbox, g.row_begin.data_ptr(), g.sq_off.data_ptr(), g.max_rows, s, r, plan.tol,
-            *(m.data_ptr() for m in quad), u.data_ptr(), v.data_ptr(), d.data_ptr(),
-            *(m.data_ptr() for m in out), plan.workspace.data_ptr(), plan.workspace_bytes,
-            plan.status.data_ptr(), stream.cuda_stream, buf)
-        hb._native.check(rc, "profiled level")
+        quad, times = plan.run_level_profiled(idx, quad, stream.cuda_stream)
         sizes = np.diff(g.begins_host)
         for i, p in enumerate(PHASES):
-            phase_ms[p] += buf[i]
+            phase_ms[p] += times[i]
             phase_flops[p] += sum(canonical_phase_flops(int(n), s, r)[p] for n in sizes)
-        quad = tuple(m[:g.nbox * r] for m in out)
     if phase_ms["apply_q_solve"] < 1e-3 * max(phase_ms.values()):
         # fused probe QR + apply-Q + solve kernel: one phase carrying both flop counts
         phase_ms["probe_qr"] += phase_ms.pop("apply_q_solve") + phase_ms.pop("panel_factors")

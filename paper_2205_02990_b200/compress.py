@@ -132,7 +132,7 @@ class CompressPlan:
     the lifted quadruple of the last compressed level (the multi-GPU hand-off)."""
 
     def __init__(self, tree: ClusterTree, s: int, rank: int, tol: float = DEFAULT_ILL_CONDITIONING_TOL,
-                 device=None, specs=None, with_root=None, out_levels=None):
+                 device=None, specs=None, with_root=None, out_levels=None, max_workspace_bytes=None):
         self.tree, self.s, self.rank, self.tol = tree, s, rank, tol
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         r = rank
@@ -142,6 +142,12 @@ class CompressPlan:
         lib = _native.lib()
         from .factorization import LevelGeometry
         self.geometry, self.first_box, self.levels = {}, {}, {}
+        # A level whose per-box scratch exceeds the cap runs in contiguous box
+        # chunks that reuse one workspace (the reference's level loop,
+        # compress.py:250-269, has no such limit on the host; config 5's leaf
+        # level needs ~110 GB of scratch at once).
+        cap = max_workspace_bytes if max_workspace_bytes is not None else _workspace_cap(dev)
+        self.chunks = {}
         ws, lift_rows = 0, []
         for level, begins, first in self.specs:
             g = LevelGeometry(begins, dev)
@@ -154,6 +160,21 @@ class CompressPlan:
                                       torch.empty(g.sq_total, dtype=f64, device=dev))
             sz = _size_t()
             _native.check(lib.hbs_level_workspace_bytes(g.nbox, g.max_rows, s, r, ctypes.byref(sz)), "workspace")
+            if sz.value > cap and g.nbox > 1:
+                per_box = sz.value / g.nbox
+                nchunk = max(1, int(cap // per_box))
+                while True:
+                    _native.check(lib.hbs_level_workspace_bytes(nchunk, g.max_rows, s, r, ctypes.byref(sz)),
+                                  "workspace")
+                    if sz.value <= cap or nchunk == 1:
+                        break
+                    nchunk = max(1, nchunk * 7 // 8)
+                parts = []
+                for b0 in range(0, g.nbox, nchunk):
+                    b1 = min(g.nbox, b0 + nchunk)
+                    parts.append((b0, b1, LevelGeometry(g.begins_host[b0:b1 + 1], dev),
+                                  torch.zeros(2 * (b1 - b0), dtype=torch.int32, device=dev)))
+                self.chunks[level] = parts
             ws = max(ws, sz.value)
             lift_rows.append(g.nbox * r)
         self.geometry[0] = LevelGeometry(np.array([0, 2 * r], dtype=np.int64), dev)
@@ -206,13 +227,51 @@ class CompressPlan:
         _native.check(rc, f"hbs_compress_level(level {level})")
         return tuple(m[:g.nbox * r] for m in out)
 
+    def run_level_profiled(self, idx, quad, stream):
+        """One level (all its chunks) with per-phase CUDA-event timing
+        (hbs_compress_level_profiled, synchronising); returns (lift outputs,
+        six phase times in ms summed over the chunks).  Measurement only."""
+        lib = _native.lib()
+        level = self.specs[idx][0]
+        r, s = self.rank, self.s
+        g = self.geometry[level]
+        u, v, d = self.levels[level]
+        out = self.lift[idx % 2]
+        buf = (ctypes.c_float * 6)()
+        total = [0.0] * 6
+        parts = self.chunks.get(level) or [(0, g.nbox, g, self._status_slices()[level])]
+        for b0, b1, geo, stat in parts:
+            row0, sq0 = int(g.begins_host[b0] - g.begins_host[0]), int(g.sq_host[b0])
+            q = [m[row0:] for m in quad]
+            rc = lib.hbs_compress_level_profiled(
+                geo.nbox, geo.row_begin.data_ptr(), geo.sq_off.data_ptr(), geo.max_rows, s, r, self.tol,
+                *(m.data_ptr() for m in q), u[row0:].data_ptr(), v[row0:].data_ptr(), d[sq0:].data_ptr(),
+                *(m[b0 * r:].data_ptr() for m in out), self.workspace.data_ptr(), self.workspace_bytes,
+                stat.data_ptr(), stream, buf)
+            _native.check(rc, f"profiled level {level}")
+            total = [a + b for a, b in zip(total, buf)]
+        return tuple(m[:g.nbox * r] for m in out), total
+
     def run(self, omega, psi, y, z, stream=None, first=0):
         """Enqueue the level sweep (compress.py:250-279) on `stream`, from spec
         index `first` (the quadruple given is that level's input)."""
         st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         quad = (omega, psi, y, z)
+        slices = self._status_slices()
         for idx in range(first, len(self.specs)):
-            quad = self.run_level(idx, quad, st)
+            level = self.specs[idx][0]
+            if level not in self.chunks:
+                quad = self.run_level(idx, quad, st)
+                continue
+            nbox = self.geometry[level].nbox
+            lvl_status = slices[level].view(2, nbox)
+            torch_stream = torch.cuda.ExternalStream(st, device=self.device) if stream is not None else None
+            out = None
+            for b0, b1, geo, cst in self.chunks[level]:
+                out = self.run_level(idx, quad, st, box_range=(b0, b1), chunk_geo=geo, status=cst)
+                with torch.cuda.stream(torch_stream) if torch_stream is not None else _nullcontext():
+                    lvl_status[:, b0:b1].copy_(cst.view(2, b1 - b0))
+            quad = out
         self.top_quad = quad
         if self.with_root:
             self.run_root(quad[0], quad[2], stream=st)
@@ -296,6 +355,23 @@ def _check_configuration(tree: ClusterTree, s: int, r: int):
                     f"probe count {s} leaves nullity {s - rows} < rank {r} for a {rows}-row node; "
                     "increase the probe count s")
             raise DimensionError(f"cannot extract {r} basis columns from a {rows} x {r} matrix")
+
+
+class _nullcontext:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _workspace_cap(dev) -> int:
+    """Per-level scratch cap: HBS_MAX_WORKSPACE_GB, else a quarter of the
+    device's memory (45 GB on a B200)."""
+    env = os.environ.get("HBS_MAX_WORKSPACE_GB")
+    if env:
+        return int(float(env) * (1 << 30))
+    return int(torch.cuda.get_device_properties(dev).total_memory // 4)
 
 
 def _device_tensor(a, device):

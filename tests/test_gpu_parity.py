@@ -325,3 +325,23 @@ def test_leaf_over_128_rows(k, r, s):
     got, want = hb.apply_matrix(f, x), O.apply(ref, x)
     assert rel(got, want) <= 1e-10
     assert rel(got, O.apply(truth, x)) <= 1e-10
+
+
+def test_chunked_levels_bitwise():
+    """A workspace cap splits levels into box chunks that reuse one scratch
+    (config 5's leaf level on one GPU); the result is bitwise the unchunked
+    sweep."""
+    c = golden_cases.load("c2_shape_twin")
+    tree = hb.build_tree(c["n"], c["leaf"])
+    quad = [torch.from_numpy(m).cuda() for m in c["samples"]]
+    full = hb.CompressPlan(tree, c["s"], c["r"])
+    full.run(*quad)
+    small = hb.CompressPlan(tree, c["s"], c["r"], max_workspace_bytes=1 << 20)
+    assert small.chunks, "the 1 MB cap must chunk the deep levels"
+    small.run(*quad)
+    torch.cuda.synchronize()
+    assert torch.equal(full.root, small.root)
+    for lvl in range(1, tree.depth + 1):
+        for a, b in zip(full.levels[lvl], small.levels[lvl]):
+            assert torch.equal(a, b)
+    assert torch.equal(full.status, small.status)
