@@ -41,6 +41,12 @@ PhaseTimer g_timer;  // only used by the profiled entry point (not thread-safe b
 
 constexpr size_t kAlign = 256;
 
+// HBS_GRAM_V3=1: the one-CTA-per-SM Gram kernel (gram.cu) instead of the TMEM one (gram_tm.cu)
+bool gram_v3() {
+  static const bool v = [] { const char* e = std::getenv("HBS_GRAM_V3"); return e && e[0] == '1'; }();
+  return v;
+}
+
 struct Carver {
   char* base;
   size_t used = 0;
@@ -175,7 +181,7 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
         G.status = status + sd * geo.nbox;
         f.side[sd].fac = w.fac[sd]; f.side[sd].fac_stride = (int64_t)nr * s;
       }
-      HBS_TRY(launch_gram(ga, nsides, st));
+      HBS_TRY(gram_v3() ? launch_gram(ga, nsides, st) : launch_gram_tm(ga, nsides, st));
       f.gflag = w.gflag;
       f.pre = 1;
       HBS_TRY(launch_probe_fused(f, nsides, st));
@@ -398,7 +404,8 @@ int hbs_gram_probe_factor(int64_t nbox, const int64_t* row_begin, int max_rows, 
   G.fac = fac; G.fac_stride = (int64_t)max_rows * s;
   G.t = t; G.t_stride = (int64_t)((max_rows + kNB - 1) / kNB) * kNB * kNB;
   G.status = status;
-  return launch_gram(ga, 1, static_cast<cudaStream_t>(stream));
+  return gram_v3() ? launch_gram(ga, 1, static_cast<cudaStream_t>(stream))
+                   : launch_gram_tm(ga, 1, static_cast<cudaStream_t>(stream));
 }
 
 int hbs_basis_qr(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows, int r,

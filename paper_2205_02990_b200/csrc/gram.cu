@@ -593,9 +593,11 @@ __global__ void __launch_bounds__(kGT, 1) gram_factor_kernel(GramArgs args) {
             if (l > k && l < nbp) z[l] = fma(-z[k], X[(j0 + l) + (j0 + k) * kLdX], z[l]);
         }
       }
-      double* tp = S.t + (size_t)b * S.t_stride + (size_t)p * kNB * kNB + (size_t)i * kNB;
+      // the fused kernel forms T from V and tau: tau_i = T_ii into row 0 of the panel's block
+      double tii = 0.0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) tp[j] = -z[j];
+      for (int j = 0; j < 32; ++j) tii = (j == i) ? -z[j] : tii;
+      S.t[(size_t)b * S.t_stride + (size_t)p * kNB * kNB + i] = tii;
     }
   }
   GR_MARK(9);

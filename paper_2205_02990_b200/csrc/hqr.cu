@@ -1703,8 +1703,20 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     // (physical warps 8..15 = logical 0..7: the arbiter favours high warp ids)
     const int lt = threadIdx.x ^ 256;
     if constexpr (PRE) {
-      if (lt == 0)
-        for (int p = 0; p < npanel; ++p) mbar_arrive(&s_ready[p]);   // every panel (and T) is final
+      // V and R are final; form each panel's compact-WY T (dlarft) from
+      // V^T V and the tau the Gram kernel left in row 0 of the panel's T block
+      for (int p = 0; p < npanel; ++p) {
+        const int j0 = p * kP, nbp = min(kP, n - j0);
+        for (int e = lt; e < nbp; e += 256) s_tau[j0 + e] = tglob[(size_t)p * kP * kP + e];
+        gsync<256>();
+        panel_gram<256>(A, lda, m, j0, nbp, G);
+        gsync<256>();
+        form_t<256>(T, Tscr, G, s_tau, j0, nbp);
+        for (int e = lt; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
+        __threadfence_block();
+        gsync<256>();
+        if (lt == 0) mbar_arrive(&s_ready[p]);
+      }
     }
     int nhh = 0;   // panels factored by the Householder chain so far (barrier parity)
     for (int p = 0; p < (PRE ? 0 : npanel); ++p) {

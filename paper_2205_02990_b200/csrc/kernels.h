@@ -117,6 +117,8 @@ struct GramArgs {
 };
 bool gram_fits(int s, int n_max, int r);
 int launch_gram(const GramArgs& args, int nsides, cudaStream_t stream);
+// Same factorisation with the LU operand in TMEM, two CTAs per SM (gram_tm.cu).
+int launch_gram_tm(const GramArgs& args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- apply Q + solve
 // Per (row tile, box, side): Yt <- Y_tile * Q (blocked WY), then

@@ -210,8 +210,8 @@ def gram_factor(blocks, s, r):
 
 @pytest.mark.parametrize("rows,s", [(128, 192), (64, 96), (32, 48), (80, 120), (16, 40)])
 def test_gram_factor_reproduces_householder(rows, s):
-    """The Gram / Householder-reconstruction factorisation (gram.cu) yields the
-    LAPACK Householder reflectors, R and panel T of Omega^T up to rounding
+    """The Gram / Householder-reconstruction factorisation (gram_tm.cu) yields
+    the LAPACK Householder reflectors, R and tau of Omega^T up to rounding
     (Householder QR is unique for dlarfg's sign rule)."""
     rng = np.random.default_rng(rows + s)
     r = s - rows
@@ -225,6 +225,8 @@ def test_gram_factor_reproduces_householder(rows, s):
         V = np.tril(fac[b].T, -1)[:, :rows] + np.eye(s, rows)
         Vref = vt[b].T
         assert np.abs(V - Vref).max() <= 1e-10
+        # tau (the diagonal of each panel's T) in row 0 of the panel's T block;
+        # the fused kernel forms T itself from V and tau
         for p in range((rows + 31) // 32):
             nbp = min(32, rows - 32 * p)
-            assert np.abs(t[b][p][:nbp, :nbp] - tt[b][p][:nbp, :nbp]).max() <= 1e-10
+            assert np.abs(t[b][p][0][:nbp] - tau[b][32 * p:32 * p + nbp]).max() <= 1e-11
