@@ -31,6 +31,13 @@ constexpr int kLdD = 17;      // diagonal-block scratch stride
 constexpr int kBk = 256;      // one 16 x 16 block
 constexpr double kFbRatio = 1e-3;
 
+#ifdef HBS_TRACE
+__device__ long long g_gtm_trace[32];
+#define GT_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_gtm_trace[i] = clock64(); } while (0)
+#else
+#define GT_MARK(i) do { } while (0)
+#endif
+
 HBS_DEV int bsw(int i, int j) { return i * 16 + (j ^ ((i & 3) << 2)); }
 HBS_DEV int bidx(int nb, int bi, int bj) { return bi * nb - bi * (bi - 1) / 2 + (bj - bi); }
 struct GR {
@@ -235,6 +242,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
   __syncthreads();
   tm_fence_after();
   const uint32_t tb = *s_tm;
+  GT_MARK(0);
 
   // ------------------------------------------------------------- G = Omega Omega^T
   // 16 x 16 units (bi <= bj) accumulate in registers, five per warp at most,
@@ -318,6 +326,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
     __syncthreads();
   }
 
+  GT_MARK(1);
   // ------------------------------------------------------------- Cholesky + Crout LU, pipelined
   double gmax = 0.0;
   for (int j = lane; j < n; j += 32) gmax = fmax(gmax, Gm.at(j, j));
@@ -370,6 +379,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
       if (warp == wu) uinv16(D16, Uinv + ol * kBk);
     }
     __syncthreads();
+    if (it == 3) GT_MARK(3);
     if (!*s_ok) {
       if (warp == 0) tm_dealloc256(tb);
       if (threadIdx.x == 0) *myflag = 1;
@@ -436,6 +446,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
       }
     }
     __syncthreads();
+    if (it == 3) GT_MARK(4);
     // (B2) LU panel 2: V1,21^T = U'11^{-T} (A rows block, cols > block), in place in
     // Ch (16 x 8 units, any warp); V1 -> fac
     const int nbl = ol >= 0 ? nb - ol - 1 : 0;
@@ -459,6 +470,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
         }
     }
     __syncthreads();
+    if (it == 3) GT_MARK(5);
     // (C) Cholesky trailing (16 x 16 units, any warp) and LU trailing (owner
     // warps): A22 -= U'12^T V1,21^T
     const int uc = nbc * (nbc + 1) / 2;
@@ -514,7 +526,10 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
       tm_wait_st();
     }
     __syncthreads();
+    if (it == 3) GT_MARK(6);
+    if (it == 2) GT_MARK(2);
   }
+  GT_MARK(7);
   // screen (the Gram squares cond(Omega); route doubtful boxes to Householder)
   if (warp == 0) {
     double lo = INFINITY, hi = 0.0;
@@ -539,6 +554,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
   }
   __syncthreads();
 
+  GT_MARK(8);
   // ------------------------------------------------------------- V2 = Omega_2^T U'^{-1}
   // V2^T = U'^{-T} Omega_2 (U'^T: lower part of A in TMEM), right-looking over
   // lane blocks with Omega_2 in shared memory (the G region; R is done):
@@ -595,6 +611,7 @@ __global__ void __launch_bounds__(kT, 2) gram_factor_tm_kernel(GramArgs args) {
     }
     __syncthreads();
   }
+  GT_MARK(9);
   if (threadIdx.x == 0) {
     *myflag = 0;
     S.status[b] = kBoxOk;
@@ -620,6 +637,15 @@ int launch_gram_tm(const GramArgs& args, int nsides, cudaStream_t stream) {
   gram_factor_tm_kernel<<<grid, kT, smem, stream>>>(args);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+extern "C" int hbs_debug_gram_tm_trace(long long* out) {
+#ifdef HBS_TRACE
+  return cudaMemcpyFromSymbol(out, g_gtm_trace, sizeof(long long) * 32) == cudaSuccess ? 0 : 4;
+#else
+  (void)out;
+  return 6;
+#endif
 }
 
 }  // namespace hbs
