@@ -1,0 +1,1265 @@
+// Device-side building blocks of the blocked Householder kernels (hqr.cu) and
+// the pipelined fused probe kernel (fused_pipe.cu): dlarfg reflectors, the
+// warp-local panel factorisations, the tensor-core block-reflector update,
+// compact-WY T, and the 32 x 32 triangular inverse.  Everything here has
+// internal linkage (each translation unit gets its own copy).
+#pragma once
+#include "common.cuh"
+#include "kernels.h"
+namespace hbs {
+
+#ifdef HBS_TRACE
+static __device__ long long g_hqr_trace[256];
+static __device__ int g_hqr_trace_mode = 0;   // record only kernels of this mode
+#define HQR_MARK(i) do { __syncthreads(); if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && args.mode == g_hqr_trace_mode) g_hqr_trace[i] = clock64(); } while (0)
+#define HQR_STEP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0) g_hqr_trace[64 + (i)] = clock64(); } while (0)
+#define FUSED_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0) g_hqr_trace[128 + (i)] = clock64(); } while (0)
+#define STEP_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 32 && lane == 0) g_hqr_trace[200 + (i)] = clock64(); } while (0)
+static __device__ long long g_pf_trace[64];
+#ifndef PF_TRACE_J0
+#define PF_TRACE_J0 0
+#endif
+#define PF_MARK(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == PF_TRACE_J0 && lane == 0) g_pf_trace[8 * warp + (i)] = clock64(); } while (0)
+static __device__ long long g_pf_step[64];
+#endif
+#if defined(HBS_TRACE) && defined(HBS_TRACE_STEP)
+// clock stamp once value v is available (warp 1 of the first panel only)
+#define PF_DEP(i, v) do { if (blockIdx.x == 0 && blockIdx.y == 0 && j0 == 0 && lane == 0 && warp == 1) { \
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(G + kP * kLdT - 1)), "d"(v) : "memory"); \
+    g_pf_step[8 * jl + (i)] = clock64(); } } while (0)
+#else
+#define PF_DEP(i, v) do { } while (0)
+#endif
+#ifndef HBS_TRACE
+#define PF_MARK(i) do { } while (0)
+#define FUSED_MARK(i) do { } while (0)
+#define STEP_MARK(i) do { } while (0)
+#define HQR_MARK(i) do { } while (0)
+#define HQR_STEP(i) do { } while (0)
+#endif
+
+namespace {
+
+constexpr int kP = 32;        // panel width (== kNB)
+constexpr int kLdT = kP + 1;  // T / G smem leading dimension
+
+struct Reflector {  // dlarfg for the current pivot
+  double tau, beta, scale;
+};
+
+HBS_DEV Reflector make_reflector(double alpha, double xn2) {
+  // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta,
+  // x <- x / (alpha - beta).  Division-free form: with rho = 1 / ||(alpha, x)||,
+  // tau = 1 + |alpha| rho and 1 / (alpha - beta) = sign(alpha) / (|alpha| + ||.||).
+  Reflector h{0.0, alpha, 0.0};
+  if (xn2 != 0.0) {
+    const double s2 = fma(alpha, alpha, xn2);
+    const double rho = rsqrt(s2);
+    const double nrm = s2 * rho;
+    h.beta = -copysign(nrm, alpha);
+    h.tau = fma(fabs(alpha), rho, 1.0);
+    h.scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+  }
+  return h;
+}
+
+// make_reflector with the reciprocal square root and the reciprocal from
+// float seeds refined by two Newton steps in double (about a tenth of the
+// issue slots of the IEEE-exact library routines, which dominate a
+// single-warp panel step); the library path covers operands outside the
+// float seed's range.
+HBS_DEV double rsqrt_nr(double a) {
+#ifndef PF_EXP_NORANGE
+  if (!(a > 1e-30 && a < 1e30)) return rsqrt(a);
+#endif
+  double y = static_cast<double>(rsqrtf(static_cast<float>(a)));
+  const double ha = 0.5 * a;
+  y = y * fma(-ha * y, y, 1.5);
+  y = y * fma(-ha * y, y, 1.5);
+  return y;
+}
+HBS_DEV double rcp_nr(double a) {
+#ifndef PF_EXP_NORANGE
+  if (!(a > 1e-30 && a < 1e30)) return __drcp_rn(a);
+#endif
+  double y = static_cast<double>(__frcp_rn(static_cast<float>(a)));
+  y = fma(y, fma(-a, y, 1.0), y);
+  y = fma(y, fma(-a, y, 1.0), y);
+  return y;
+}
+HBS_DEV Reflector make_reflector_fast(double alpha, double xn2) {
+  Reflector h{0.0, alpha, 0.0};
+  if (xn2 != 0.0) {
+    const double s2 = fma(alpha, alpha, xn2);
+    const double rho = rsqrt_nr(s2);
+    const double nrm = s2 * rho;
+    h.beta = -copysign(nrm, alpha);
+    h.tau = fma(fabs(alpha), rho, 1.0);
+    h.scale = copysign(rcp_nr(fabs(alpha) + nrm), alpha);
+  }
+  return h;
+}
+
+// V(i, q) of panel j0: unit lower trapezoidal, stored in A's panel columns
+// (tails already scaled).  q >= nbp -> 0.
+HBS_DEV double vval(const double* A, int lda, int j0, int nbp, int i, int q) {
+  const int c = j0 + q;
+  if (q >= nbp || i < c) return 0.0;
+  return i == c ? 1.0 : A[i + c * lda];
+}
+
+// Fetch W(p, g) (p = kk + t) from C-fragments acc[f][e] (row g', col 2t'+e)
+// into the B-fragment layout (row t, col g) of k-step kk.
+template <int NF>
+HBS_DEV double cfrag_to_bfrag(const double (&acc)[NF][2], int kk, int lane) {
+  // kk is a compile-time constant in every (unrolled) caller, so acc[kk >> 3]
+  // resolves to registers and only two shuffles are issued.
+  const int g = lane >> 2, t = lane & 3;
+  const int src = 4 * ((kk & 7) + t) + (g >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, acc[kk >> 3][0], src);
+  const double v1 = __shfl_sync(0xffffffffu, acc[kk >> 3][1], src);
+  return (g & 1) ? v1 : v0;
+}
+
+// Warp-group synchronisation: NTG == 0 means the whole CTA (__syncthreads),
+// otherwise named barrier 1 over the first NTG threads.
+template <int NTG>
+HBS_DEV void gsync() {
+  if (NTG == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;\n" ::"n"(NTG) : "memory");
+}
+template <int NTG>
+HBS_DEV int gthreads() { return NTG == 0 ? (int)blockDim.x : NTG; }
+// Logical thread index of a warp group.  In the fused kernel (NTG == 256) the
+// latency-critical panel group runs on physical warps 8..15, which the warp
+// arbiter favours (highest warp id first), so logical = physical ^ 256.
+template <int NTG>
+HBS_DEV int ltid() { return NTG == 256 ? (int)(threadIdx.x ^ 256u) : (int)threadIdx.x; }
+
+// A(j0:m, cb:ce) <- (I - V op(T) V^T) A(j0:m, cb:ce), V = panel j0 (nbp cols),
+// op(T) = T^T when trans (dgeqrf trailing update, H^T from the left), else T
+// (dorgqr).  T in smem (kP x kLdT).  mpad = rows rounded up to 8 (zero rows).
+template <int NTG>
+HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp, const double* T, bool trans,
+                                   int cb, int ce, int ldt = kLdT, int warp_base = 0) {
+  const int warp = (ltid<NTG>() >> 5) - warp_base, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nstrip = (ce - cb + 7) >> 3;
+  for (int sidx = warp; sidx < nstrip; sidx += nw) {
+    const int c0 = cb + 8 * sidx;
+    const bool colok = c0 + g < ce;
+    // GEMM1: W = V^T A_strip  (32 x 8), K = rows j0 .. mpad
+    double w[4][2] = {};
+    for (int k = j0; k < mpad; k += 4) {
+      const double bv = colok ? A[(k + t) + (c0 + g) * lda] : 0.0;
+      if (k < j0 + kP) {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) dmma8x8x4(w[f][0], w[f][1], vval(A, lda, j0, nbp, k + t, 8 * f + g), bv);
+      } else {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const double av = (8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0;
+          dmma8x8x4(w[f][0], w[f][1], av, bv);
+        }
+      }
+    }
+    // GEMM2: W2 = op(T) W (32 x 8)
+    double w2[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const double bv = cfrag_to_bfrag<4>(w, kk, lane);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int row = 8 * f + g, col = kk + t;
+        const double av = trans ? T[col * ldt + row] : T[row * ldt + col];
+        dmma8x8x4(w2[f][0], w2[f][1], av, bv);
+      }
+    }
+    double bneg[kP / 4];
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) bneg[kk / 4] = -cfrag_to_bfrag<4>(w2, kk, lane);
+    // GEMM3: A_strip -= V W2, 8-row blocks, four in flight
+    const int col0 = c0 + 2 * t;
+    const bool ok0 = col0 < ce, ok1 = col0 + 1 < ce;
+    for (int ib = j0; ib < mpad; ib += 32) {
+      double cv[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ib + 8 * u + g;
+        const bool rok = ib + 8 * u < mpad;
+        cv[u][0] = (ok0 && rok) ? A[i + col0 * lda] : 0.0;
+        cv[u][1] = (ok1 && rok) ? A[i + (col0 + 1) * lda] : 0.0;
+      }
+      if (ib < j0 + kP) {
+#pragma unroll
+        for (int kk = 0; kk < kP; kk += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            dmma8x8x4(cv[u][0], cv[u][1], vval(A, lda, j0, nbp, ib + 8 * u + g, kk + t), bneg[kk / 4]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kP; kk += 4) {
+          const bool qok = kk + t < nbp;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double av = qok ? A[(ib + 8 * u + g) + (j0 + kk + t) * lda] : 0.0;
+            dmma8x8x4(cv[u][0], cv[u][1], av, bneg[kk / 4]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ib + 8 * u + g;
+        if (ib + 8 * u < mpad) {
+          if (ok0) A[i + col0 * lda] = cv[u][0];
+          if (ok1) A[i + (col0 + 1) * lda] = cv[u][1];
+        }
+      }
+    }
+  }
+}
+
+// Factor panel j0 (nbp <= 32 columns) in place.  Leaves: pre-scale reflector
+// values in A (finalised afterwards by the caller), tau/scale/beta in smem,
+// G(c, j) = v_c . v_j (c < j) in G.
+// Panel factorisation in 8-column sub-panels.  In sub-panel q, warp w < 8 owns
+// column cs + w (cs = j0 + 8q) in registers (rows j0 + lane + 32k).  Step j
+// needs only pivot j: its owner publishes (column in A, tau/scale/beta in
+// smem) and arrives on bar[j]; the others wait on bar[j] alone.  bar[] completes
+// once per panel (parity = panel & 1).  The owners of earlier sub-panel columns
+// form the compact-WY dots v_c . v_j on the fly (G8); after the 8 steps the
+// sub-panel's block reflector is applied to the rest of the panel on the
+// tensor cores, so only 8 warps ever contend for issue during a step.
+template <int MR, int NTG>
+HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                          double* s_beta, uint64_t* bar, unsigned parity, double* G8, double* T8,
+                          double* wpart, double* wfin) {
+  constexpr int kSub = 8;
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
+  for (int cs = j0; cs < j0 + nbp; cs += kSub) {
+    const int nsub = min(kSub, j0 + nbp - cs);
+    const int jq = cs - j0;           // step index of the sub-panel's first pivot
+    if (warp < nsub) {
+      const int c = cs + warp;
+      double x[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) x[k] = (k < kc) ? A[(j0 + lane + 32 * k) + c * lda] : 0.0;
+      if (warp == 0) {  // first pivot of the sub-panel: exact norm
+        double p = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          const int row = j0 + lane + 32 * k;
+          if (k < kc && row > cs) p = fma(x[k], x[k], p);
+        }
+        p = warp_sum(p);
+        const double alpha = __shfl_sync(0xffffffffu, x[0], jq);   // row cs: slot 0, lane jq (< 32)
+        if (lane == 0) {
+          const Reflector h = make_reflector(alpha, p);
+          s_tau[cs] = h.tau; s_scale[cs] = h.scale; s_beta[cs] = h.beta;
+          mbar_arrive(&bar[jq]);
+          HQR_STEP(jq);
+        }
+      }
+      for (int i = 0; i < nsub; ++i) {
+        const int jj = cs + i, j = jq + i;
+        if (c == jj) continue;
+        mbar_wait(&bar[j], parity);
+        const double tau = s_tau[jj], scale = s_scale[jj];
+        double pv[MR];
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          const int row = j0 + lane + 32 * k;
+          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+        }
+        const bool pub = (c == jj + 1);   // I publish the next pivot
+        double d = 0.0, sxx = 0.0, spp = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          d = fma(pv[k], x[k], d);
+          if (pub) {
+            const int row = j0 + lane + 32 * k;
+            if (row > jj + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
+          }
+        }
+        const double rj = __shfl_sync(0xffffffffu, x[0], j);   // my value in row jj (slot 0, lane j < 32)
+        double xn_old = 0.0, pn = 0.0;
+        if (pub) {
+          pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+          xn_old = __shfl_sync(0xffffffffu, x[0], j + 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (pub) {
+            sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+            spp += __shfl_xor_sync(0xffffffffu, spp, o);
+          }
+        }
+        if (c < jj) {   // compact-WY dot v_c . v_jj (my column is a retired reflector)
+          if (lane == 0) G8[(c - cs) * kSub + i] = s_scale[c] * (rj + scale * d);
+          continue;
+        }
+        const double f = tau * (rj + scale * d), gs = f * scale;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) x[k] = fma(-gs, pv[k], x[k]);
+        if (lane == j) x[0] -= f;
+        if (pub) {
+          const double sxp = d - pn * xn_old;
+          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
+          if (!(nrm > 0.5 * sxx) || sxx == 0.0) {   // cancellation: recompute exactly
+            double p = 0.0;
+#pragma unroll
+            for (int k = 0; k < MR; ++k) {
+              const int row = j0 + lane + 32 * k;
+              if (k < kc && row > jj + 1) p = fma(x[k], x[k], p);
+            }
+            nrm = warp_sum(p);
+          }
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
+          const double alpha = __shfl_sync(0xffffffffu, x[0], j + 1);
+          __syncwarp();
+          if (lane == 0) {
+            const Reflector h = make_reflector(alpha, nrm);
+            s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+            mbar_arrive(&bar[j + 1]);
+            HQR_STEP(j + 1);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
+    }
+    gsync<NTG>();
+    if (ltid<NTG>() == 0) HQR_STEP(40 + (jq >> 3) * 4);
+    // finalise the sub-panel: v tails = x * scale, diagonal = beta
+    for (int q = 0; q < nsub; ++q) {
+      const int c = cs + q;
+      const double sc = s_scale[c];
+      for (int i = c + ltid<NTG>(); i < m; i += gthreads<NTG>()) {
+        if (i > c) A[i + c * lda] *= sc;
+        else A[i + c * lda] = s_beta[c];
+      }
+    }
+    const int c1 = cs + kSub, c2 = j0 + nbp;   // remaining panel columns
+    if (c1 < c2) {
+      // T8 (dlarft recurrence, lanes 0..7 of warp 0); meanwhile warps 1..4
+      // form partial W = V_sub^T X_rest over K chunks.
+      if (warp == 0) {
+        if (lane < kSub) {
+          double trow[kSub];
+#pragma unroll
+          for (int cc = 0; cc < kSub; ++cc) {
+            const double tc = (cc < nsub) ? s_tau[cs + cc] : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < cc; ++q)
+              if (q >= lane) acc = fma(trow[q], G8[q * kSub + cc], acc);
+            trow[cc] = (lane < cc) ? -tc * acc : (lane == cc ? tc : 0.0);
+          }
+#pragma unroll
+          for (int cc = 0; cc < kSub; ++cc) T8[lane * kSub + cc] = trow[cc];
+        }
+      }
+      gsync<NTG>();   // finalised V visible
+      if (ltid<NTG>() == 0) HQR_STEP(41 + (jq >> 3) * 4);
+      const int kspan = round_up(m - cs, 4);
+      const int nsplit = 4;
+      const int kchunk = round_up((kspan + nsplit - 1) / nsplit, 4);
+      if (warp >= 1 && warp <= nsplit) {
+        const int ws = warp - 1;
+        const int kb = cs + ws * kchunk, ke = min(cs + kspan, kb + kchunk);
+        double w[3][2] = {};
+        for (int k = kb; k < ke; k += 4) {
+          const int i = k + t;
+          // A = V_sub^T (row g = reflector, col = row index i)
+          const double av = (g < nsub && i >= cs + g) ? (i == cs + g ? 1.0 : A[i + (cs + g) * lda]) : 0.0;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const int cc = c1 + 8 * f + g;
+            const double bv = cc < c2 ? A[i + cc * lda] : 0.0;
+            dmma8x8x4(w[f][0], w[f][1], av, bv);
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          wpart[ws * 192 + g * 24 + 8 * f + 2 * t] = w[f][0];
+          wpart[ws * 192 + g * 24 + 8 * f + 2 * t + 1] = w[f][1];
+        }
+      }
+      gsync<NTG>();
+      if (ltid<NTG>() == 0) HQR_STEP(42 + (jq >> 3) * 4);
+      // W' = T8^T (sum of partials)  (8 x 24)
+      for (int e = ltid<NTG>(); e < 192; e += gthreads<NTG>()) {
+        const int q = e / 24, cc = e % 24;
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < kSub; ++a) {
+          const double wa = wpart[a * 24 + cc] + wpart[192 + a * 24 + cc] + wpart[384 + a * 24 + cc] +
+                            wpart[576 + a * 24 + cc];
+          acc = fma(T8[a * kSub + q], wa, acc);
+        }
+        wfin[e] = acc;
+      }
+      gsync<NTG>();
+      // X_rest(rows cs.., c1..c2) -= V_sub W'
+      const int nrb = (round_up(m, 8) - cs + 7) >> 3;
+      for (int u = warp; u < nrb * 3; u += nw) {
+        const int rbk = u / 3, f = u % 3;
+        const int i = cs + 8 * rbk + g;
+        const int col = c1 + 8 * f + 2 * t;
+        if (c1 + 8 * f >= c2) continue;
+        double c0v = (col < c2) ? A[i + col * lda] : 0.0;
+        double c1v = (col + 1 < c2) ? A[i + (col + 1) * lda] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kSub; kk += 4) {
+          const int q = kk + t;
+          const double av = (q < nsub && i >= cs + q) ? (i == cs + q ? 1.0 : A[i + (cs + q) * lda]) : 0.0;
+          const double bv = -wfin[q * 24 + 8 * f + g];
+          dmma8x8x4(c0v, c1v, av, bv);
+        }
+        if (col < c2) A[i + col * lda] = c0v;
+        if (col + 1 < c2) A[i + (col + 1) * lda] = c1v;
+      }
+    }
+    gsync<NTG>();
+    if (ltid<NTG>() == 0) HQR_STEP(43 + (jq >> 3) * 4);
+  }
+}
+
+// Whole-panel factorisation (no sub-panels).  NW warps; warp w owns panel
+// columns j0 + w + NW*u (u < CPW = 32/NW) in registers (rows j0 + lane + 32k).
+// Step j needs only pivot j: its owner publishes (column in A; tau / scale /
+// beta in smem; next-pivot norm by the expansion
+// ||x - g p||^2 = sxx - 2 g sxp + g^2 spp, recomputed exactly on
+// cancellation) and arrives on bar[j]; every other warp waits on bar[j] only.
+// Owners of retired columns form the compact-WY dots G(c, j) = v_c . v_j in
+// the same reductions, so T needs no separate Gram.  bar[] completes once per
+// panel (parity = panel & 1).
+template <int MR, int NW, int NTG>
+HBS_DEV void panel_factor_wide(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                               double* s_beta, uint64_t* bar, unsigned parity, double* G) {
+  // G(q, j) is only written for q < j < nbp; zero it so form_t never reads
+  // stale shared memory for partial panels.
+  for (int e = ltid<NTG>(); e < kP * kLdT; e += gthreads<NTG>()) G[e] = 0.0;
+  gsync<NTG>();
+  constexpr int CPW = 32 / NW;
+  const int warp = (ltid<NTG>() >> 5), lane = ltid<NTG>() & 31;
+  const int kc = (m - j0 + 31) >> 5;
+  double x[CPW][MR];
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int q = warp + NW * u;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) x[u][k] = (q < nbp && k < kc) ? A[(j0 + lane + 32 * k) + (j0 + q) * lda] : 0.0;
+  }
+  if (warp == 0) {  // first pivot: column j0 (warp 0, u = 0), exact norm
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < MR; ++k)
+      if (k < kc && j0 + lane + 32 * k > j0) p = fma(x[0][k], x[0][k], p);
+    p = warp_sum(p);
+    const double alpha = __shfl_sync(0xffffffffu, x[0][0], 0);
+    if (lane == 0) {
+      const Reflector h = make_reflector(alpha, p);
+      s_tau[j0] = h.tau; s_scale[j0] = h.scale; s_beta[j0] = h.beta;
+      mbar_arrive(&bar[0]);
+    }
+  }
+  for (int j = 0; j < nbp; ++j) {
+    const int jj = j0 + j;
+    const bool tr = (j == 6) && (((j + 1) % NW) == warp);
+    if (tr) STEP_MARK(0);
+    mbar_wait(&bar[j], parity);
+    if (tr) STEP_MARK(1);
+    const double tau = s_tau[jj], scale = s_scale[jj];
+    double pv[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int row = j0 + lane + 32 * k;
+      pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+    }
+    const bool pubw = (j + 1 < nbp) && (((j + 1) % NW) == warp);   // I own the next pivot
+    const int upub = (j + 1) / NW;
+    double d[CPW], r_[CPW];
+    double sxx = 0.0, spp = 0.0;
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      r_[u] = __shfl_sync(0xffffffffu, x[u][0], j);
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) a = fma(pv[k], x[u][k], a);
+      d[u] = a;
+      if (pubw && u == upub) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (j0 + lane + 32 * k > jj + 1) { sxx = fma(x[u][k], x[u][k], sxx); spp = fma(pv[k], pv[k], spp); }
+      }
+    }
+    if (tr) STEP_MARK(2);
+    double pn = 0.0, xn_old = 0.0;
+    if (pubw) {
+      pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+#pragma unroll
+      for (int u = 0; u < CPW; ++u)
+        if (u == upub) xn_old = __shfl_sync(0xffffffffu, x[u][0], j + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+      if (pubw) {
+        sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+        spp += __shfl_xor_sync(0xffffffffu, spp, o);
+      }
+    }
+    if (tr) STEP_MARK(3);
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const int q = warp + NW * u, c = j0 + q;
+      if (q >= nbp || c == jj) continue;
+      if (c < jj) {   // retired reflector: compact-WY dot v_c . v_jj
+        if (lane == 0) G[q * kLdT + j] = s_scale[c] * (r_[u] + scale * d[u]);
+        continue;
+      }
+      const double f = tau * (r_[u] + scale * d[u]), gs = f * scale;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) x[u][k] = fma(-gs, pv[k], x[u][k]);
+      if (lane == j) x[u][0] -= f;
+      if (pubw && u == upub) {
+        if (tr) STEP_MARK(4);
+        const double sxp = d[u] - pn * xn_old;
+        double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
+        if (!(nrm > 0.5 * sxx) || sxx == 0.0) {   // cancellation: recompute exactly
+          double p = 0.0;
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (k < kc && j0 + lane + 32 * k > jj + 1) p = fma(x[u][k], x[u][k], p);
+          nrm = warp_sum(p);
+        }
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[u][k];
+        if (tr) STEP_MARK(5);
+        const double alpha = __shfl_sync(0xffffffffu, x[u][0], j + 1);
+        __syncwarp();
+        if (lane == 0) {
+          const Reflector h = make_reflector(alpha, nrm);
+          s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
+          if (tr) STEP_MARK(6);
+          mbar_arrive(&bar[j + 1]);
+          if (tr) STEP_MARK(7);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int q = warp + NW * u;
+    if (q < nbp) {
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (k < kc) A[(j0 + lane + 32 * k) + (j0 + q) * lda] = x[u][k];
+    }
+  }
+  gsync<NTG>();
+  for (int q = 0; q < nbp; ++q) {   // finalise: v tails = x * scale, diagonal = beta
+    const int c = j0 + q;
+    const double sc = s_scale[c];
+    for (int i = c + ltid<NTG>(); i < m; i += gthreads<NTG>()) {
+      if (i > c) A[i + c * lda] *= sc;
+      else A[i + c * lda] = s_beta[c];
+    }
+  }
+  gsync<NTG>();
+}
+
+// Panel factorisation with 8-lane column groups (warps 0..7 of the CTA).
+// Lane group lg = lane / 8 of warp w owns panel column q = 4w + lg; lane
+// li = lane % 8 of the group holds rows j0 + li + 8k (k < MR8) in registers.
+// Every column-dot reduction is a 3-stage xor shuffle inside the group, and
+// the four groups of a warp reduce in the same shuffle instructions.  Step j
+// needs only pivot j (mbarrier hand-off from the warp owning it); a step is
+// bound by the FP64 and shuffle/shared pipes the active warps share, so warp
+// w stops after step 4w+3 (its columns are all reflectors by then) and only
+// the publishing warp runs the next pivot's norm.  The compact-WY dots
+// V^T V for form_t come from one tensor-core Gram product afterwards.
+template <int NTG>
+HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G);
+
+// Transposed butterfly: four per-lane partial sums -> on return lanes
+// 8s .. 8s+7 hold the warp-wide sum of slot s = lane >> 3 (6 shuffles, 5 stages).
+HBS_DEV double reduce4_t(const double (&a)[4], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8;
+  const double k0 = (b4 ? a[2] : a[0]) + __shfl_xor_sync(0xffffffffu, b4 ? a[0] : a[2], 16);
+  const double k1 = (b4 ? a[3] : a[1]) + __shfl_xor_sync(0xffffffffu, b4 ? a[1] : a[3], 16);
+  double k = (b3 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;
+}
+
+// Panel factorisation with warp-local column blocks (warps 0..7 of the group).
+// Warp w holds panel columns 4w .. 4w+3 in registers, lane l rows j0 + l + 32k.
+// It first applies the reflectors of the earlier warps' columns as they are
+// published (mbarrier per reflector, one step behind the producer), then
+// factors its own four columns with no cross-warp traffic: a step is the
+// pivot's dots, one transposed 4-slot butterfly, the rank-1 update and the
+// next pivot's norm by the update formula (exact recomputation on
+// cancellation), so only every fourth pivot crosses warps.  Published
+// columns hold the final R entries, beta and the dlarfg-scaled tails; the
+// compact-WY dots V^T V for form_t come from one tensor-core Gram product.
+template <int MR, int NTG>
+HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                            double* s_beta, uint64_t* bar, unsigned parity, double* G, uint64_t* pub = nullptr) {
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31;
+  if (warp < ((nbp + 3) >> 2)) {
+    const int cb = 4 * warp;     // my first panel column
+    const int mr = m - j0;       // panel rows; relative row of (lane, k) = lane + 32 k
+    double x[4][MR];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        x[c][k] = (cb + c < nbp && row < mr) ? A[(j0 + row) + (j0 + cb + c) * lda] : 0.0;
+      }
+    PF_MARK(0);
+    // reflectors 0 .. cb-1 (earlier warps), applied as they are published
+    for (int j = 0; j < cb; ++j) {
+#ifdef PF_EXP_SLEEP
+      mbar_wait_sleep(&bar[j], parity);
+#else
+      mbar_wait(&bar[j], parity);
+#endif
+      const double tau = s_tau[j0 + j];
+      double v[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        v[k] = (k > 0 || row > j) ? (row < mr ? A[(j0 + row) + (j0 + j) * lda] : 0.0) : (row == j ? 1.0 : 0.0);
+      }
+      double pc[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          if (k & 1) a1 = fma(v[k], x[c][k], a1);
+          else a0 = fma(v[k], x[c][k], a0);
+        }
+        pc[c] = a0 + a1;
+      }
+      const double tot = tau * reduce4_t(pc, lane);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double w = __shfl_sync(0xffffffffu, tot, 8 * c);
+#pragma unroll
+        for (int k = 0; k < MR; ++k) x[c][k] = fma(-w, v[k], x[c][k]);
+      }
+    }
+    PF_MARK(1);
+    // my first pivot: exact norm below row cb, alpha = row cb (lane cb, slot 0)
+    double nrm, alpha;
+    {
+      double pp = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (k > 0 || lane > cb) pp = fma(x[0][k], x[0][k], pp);
+      nrm = warp_sum(pp);
+      alpha = __shfl_sync(0xffffffffu, x[0][0], cb);
+    }
+    PF_MARK(2);
+    // publish column j: R above, beta on the diagonal, scaled tail below
+    auto publish = [&](int j, const Reflector& hh, const double (&xc)[MR]) {
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int row = lane + 32 * k;
+        if (row < mr) A[(j0 + row) + (j0 + j) * lda] = row < j ? xc[k] : (row == j ? hh.beta : xc[k] * hh.scale);
+      }
+      if (lane == 0) { s_tau[j0 + j] = hh.tau; s_scale[j0 + j] = hh.scale; s_beta[j0 + j] = hh.beta; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[j]);
+    };
+    Reflector hp{0.0, 0.0, 0.0};
+    double xp[MR];
+    int pubc = -1;
+#pragma unroll
+    for (int jl = 0; jl < 4; ++jl) {
+      const int j = cb + jl;
+      if (j >= nbp) break;
+      PF_DEP(0, 0.0);
+#ifdef PF_EXP_NOREFL
+      const Reflector h{1.5 + 1e-300 * alpha, alpha, 0.5 + 1e-300 * nrm};
+#elif defined(PF_EXP_FASTREFL)
+      const Reflector h = make_reflector_fast(alpha, nrm);
+#else
+      const Reflector h = make_reflector(alpha, nrm);
+#endif
+#ifndef PF_EXP_NOPUB
+      if (pubc >= 0) { publish(cb + pubc, hp, xp); pubc = -1; }
+#endif
+      double pv[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) pv[k] = (k > 0 || lane > j) ? x[jl][k] : 0.0;   // j < 32
+      double pc[4] = {0.0, 0.0, 0.0, 0.0}, r[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = jl + 1; c < 4; ++c) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          if (k & 1) a1 = fma(pv[k], x[c][k], a1);
+          else a0 = fma(pv[k], x[c][k], a0);
+        }
+        pc[c] = a0 + a1;
+        r[c] = __shfl_sync(0xffffffffu, x[c][0], j);   // row j of column c
+      }
+      // next pivot (column jl+1): ||x||^2, ||pv||^2 over rows > j+1, row j+1 values
+      double sxx = 0.0, spp = 0.0, xn_old = 0.0, pn = 0.0;
+      if (jl < 3) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k)
+          if (k > 0 || lane > j + 1) { sxx = fma(x[jl + 1][k], x[jl + 1][k], sxx); spp = fma(pv[k], pv[k], spp); }
+        xn_old = __shfl_sync(0xffffffffu, x[jl + 1][0], j + 1);
+        pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
+      }
+      PF_DEP(1, pc[3] + r[3] + sxx + spp);
+      const double dsum = reduce4_t(pc, lane);
+      PF_DEP(2, dsum);
+      PF_DEP(3, h.tau * h.scale);
+      if (jl < 3) { sxx = warp_sum(sxx); spp = warp_sum(spp); }
+      double gsn = 0.0, dn = 0.0;
+#pragma unroll
+      for (int c = jl + 1; c < 4; ++c) {
+        const double dc = __shfl_sync(0xffffffffu, dsum, 8 * c);
+        const double f = h.tau * (r[c] + h.scale * dc), gs = f * h.scale;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) x[c][k] = fma(-gs, pv[k], x[c][k]);
+        if (lane == j) x[c][0] -= f;
+        if (c == jl + 1) { gsn = gs; dn = dc; }
+      }
+      PF_DEP(4, x[3][0] + x[3][MR - 1]);
+      if (jl < 3 && j + 1 < nbp) {
+        // ||x'||^2 = sxx - 2 gs (x . pv) + gs^2 spp over rows > j+1
+        double nn = fma(gsn * gsn, spp, fma(-2.0 * gsn, dn - pn * xn_old, sxx));
+        alpha = fma(-gsn, pn, xn_old);
+#ifndef PF_EXP_NONEED
+        if (!(nn > 0.5 * sxx) || sxx == 0.0) {   // warp-uniform
+          double pp = 0.0;
+#pragma unroll
+          for (int k = 0; k < MR; ++k)
+            if (k > 0 || lane > j + 1) pp = fma(x[jl + 1][k], x[jl + 1][k], pp);
+          nn = warp_sum(pp);
+        }
+#endif
+        nrm = nn;
+      }
+      PF_DEP(5, nrm + alpha);
+      // column j is published at the top of the next step (after that
+      // step's reflector is issued) or after the loop
+#ifdef PF_EXP_DEFER
+      hp = h;
+      pubc = jl;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) xp[k] = x[jl][k];
+#else
+      publish(j, h, x[jl]);
+#endif
+      PF_MARK(3 + jl);
+      PF_DEP(6, 0.0);
+    }
+    if (pubc >= 0) publish(cb + pubc, hp, xp);
+  }
+  __threadfence_block();
+  gsync<NTG>();
+  // every reflector of the panel is in A: the pipelined kernel's group Y starts
+  // the look-ahead product on it while T is formed
+  if (pub != nullptr && ltid<NTG>() == 0) mbar_arrive(pub);
+  panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
+  gsync<NTG>();
+}
+
+template <int MR8, int NTG>
+HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
+                            double* s_beta, uint64_t* bar, unsigned parity, double* G, double* s_an) {
+  // s_an[j] = alpha (pre-reflection diagonal), s_an[32 + j] = ||x||^2 of pivot j:
+  // the publisher stores only these; every warp forms the reflector itself,
+  // overlapped with its own loads and reductions (off the critical chain).
+  const int warp = (ltid<NTG>() >> 5), lane = ltid<NTG>() & 31;
+  if (warp < 8) {
+    const int lg = lane >> 3, li = lane & 7, gbase = lane & 24;
+    // contiguous columns per warp: warp w retires after step 4w+3 and leaves
+    // the pipes to the warps still updating
+    const int q = 4 * warp + lg, c = j0 + q, jlast = 4 * warp + 3;
+    const bool own = q < nbp;
+    const int kc = (m - j0 + 7) >> 3;
+    double x[MR8];
+#pragma unroll
+    for (int k = 0; k < MR8; ++k) x[k] = (own && k < kc) ? A[(j0 + li + 8 * k) + c * lda] : 0.0;
+    if (warp == 0) {  // first pivot j0 = column q 0 (warp 0, group 0): exact norm
+      double p = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR8; ++k)
+        if (k < kc && li + 8 * k > 0) p = fma(x[k], x[k], p);
+      p += __shfl_xor_sync(0xffffffffu, p, 4);
+      p += __shfl_xor_sync(0xffffffffu, p, 2);
+      p += __shfl_xor_sync(0xffffffffu, p, 1);
+      const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
+      if (lane == 0) {
+        s_an[0] = alpha; s_an[32] = p;
+        mbar_arrive(&bar[0]);
+      }
+    }
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {          // row slot of the pivot: kb = j / 8 (compile time)
+      for (int jl = 0; jl < 8; ++jl) {
+        const int j = 8 * kb + jl, jj = j0 + j;
+        if (j >= nbp || j > jlast) break;
+        const bool tr = (j == 6) && own && (q == 7) && li == 0;
+        // warp-uniform: this warp owns pivot j+1 (group (j+1)%4 of warp (j+1)/4).
+        // Only it runs the norm / publish work and its shuffles: the SM's
+        // shuffle and shared-memory pipes, shared by the eight warps, bound a step.
+        const bool pubw = warp == ((j + 1) >> 2) && j + 1 < nbp;
+        mbar_wait(&bar[j], parity);
+        if (tr) STEP_MARK(0);
+        double pv[MR8];
+#pragma unroll
+        for (int k = 0; k < MR8; ++k) {
+          const int row = j0 + li + 8 * k;
+          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
+        }
+        const Reflector hj = make_reflector(s_an[j], s_an[32 + j]);
+        const double tau = hj.tau, scale = hj.scale;
+        if (tr) STEP_MARK(1);
+        if (c == jj && li == 0) { s_tau[jj] = hj.tau; s_scale[jj] = hj.scale; s_beta[jj] = hj.beta; }
+        if (tr) STEP_MARK(2);
+        const bool pub = own && (q == j + 1);
+        // my value in row jj (slot kb, lane jl of my group)
+        const double r = __shfl_sync(0xffffffffu, x[kb], gbase | jl);
+        double dd[8] = {};
+#pragma unroll
+        for (int k = 0; k < MR8; ++k) dd[k & 7] = fma(pv[k], x[k], dd[k & 7]);
+        if (tr) STEP_MARK(3);
+        double d = ((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]));
+        // publisher warp: ||x||^2 and ||pv||^2 over rows > jj+1 (pre-update x),
+        // and the row-(jj+1) values of x and pv
+        double sxx = 0.0, spp = 0.0, xn_old = 0.0, pn = 0.0;
+        if (pubw) {
+          double sx[4] = {}, sp[4] = {};
+#pragma unroll
+          for (int k = 0; k < MR8; ++k)
+            if (li + 8 * k > j + 1) { sx[k & 3] = fma(x[k], x[k], sx[k & 3]); sp[k & 3] = fma(pv[k], pv[k], sp[k & 3]); }
+          sxx = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+          spp = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+          const int nl = (jl == 7) ? gbase : (gbase | (jl + 1));
+          xn_old = __shfl_sync(0xffffffffu, (jl == 7) ? x[kb < 3 ? kb + 1 : kb] : x[kb], nl);
+          pn = __shfl_sync(0xffffffffu, (jl == 7) ? pv[kb < 3 ? kb + 1 : kb] : pv[kb], nl);
+        }
+        d += __shfl_xor_sync(0xffffffffu, d, 4);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        if (tr) STEP_MARK(4);
+        const double f = tau * (r + scale * d), gs = f * scale;
+        if (own && c > jj) {
+#pragma unroll
+          for (int k = 0; k < MR8; ++k) x[k] = fma(-gs, pv[k], x[k]);
+          if (li == jl) x[kb] -= f;
+        }
+        if (tr) STEP_MARK(5);
+        if (pubw) {
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 4);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 4);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 2);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 2);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, 1);
+          spp += __shfl_xor_sync(0xffffffffu, spp, 1);
+          // next pivot: ||x'||^2 over rows > jj+1 = sxx - 2 gs sxp + gs^2 spp,
+          // recomputed exactly on cancellation; alpha = updated row jj+1
+          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, d - pn * xn_old, sxx));
+          const double alpha = fma(-gs, pn, xn_old);
+          if (tr) STEP_MARK(6);
+          const bool need = pub && (!(nrm > 0.5 * sxx) || sxx == 0.0);
+          if (__any_sync(0xffffffffu, need)) {
+            double pp = 0.0;
+#pragma unroll
+            for (int k = 0; k < MR8; ++k)
+              if (k < kc && li + 8 * k > j + 1) pp = fma(x[k], x[k], pp);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 4);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 2);
+            pp += __shfl_xor_sync(0xffffffffu, pp, 1);
+            if (need) nrm = pp;
+          }
+          if (tr) STEP_MARK(7);
+          if (pub) {
+#pragma unroll
+            for (int k = 0; k < MR8; ++k)
+              if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
+          }
+          __syncwarp();
+          if (pub && li == 0) {
+            s_an[j + 1] = alpha; s_an[32 + j + 1] = nrm;
+            if (tr) STEP_MARK(8);
+            mbar_arrive(&bar[j + 1]);
+            if (tr) STEP_MARK(9);
+          }
+        }
+      }
+    }
+    if (own) {
+#pragma unroll
+      for (int k = 0; k < MR8; ++k)
+        if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
+    }
+  }
+  gsync<NTG>();
+  for (int qq = 0; qq < nbp; ++qq) {   // finalise: v tails = x * scale, diagonal = beta
+    const int cc = j0 + qq;
+    const double sc = s_scale[cc];
+    for (int i = cc + ltid<NTG>(); i < m; i += gthreads<NTG>()) {
+      if (i > cc) A[i + cc * lda] *= sc;
+      else A[i + cc * lda] = s_beta[cc];
+    }
+  }
+  gsync<NTG>();
+  panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
+  gsync<NTG>();
+}
+
+// G = V_p^T V_p (32 x 32) on the tensor cores; warp w < 16 computes one 8x8 block.
+template <int NTG>
+HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G) {
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int kend = round_up(m, 4);
+  for (int blk = warp; blk < 16; blk += nw) {
+    const int fi = blk >> 2, fj = blk & 3;
+    if (fi > fj) continue;  // only blocks on/above the diagonal are used
+    // four independent accumulator chains (k-steps interleaved); rows above
+    // j0 + 8 fj are zero in column block fj
+    double c[4][2] = {};
+    int k = j0 + 8 * fj;
+    for (; k < j0 + kP && k < kend; k += 4) {
+      const int i = k + t;
+      dmma8x8x4(c[(k >> 2) & 3][0], c[(k >> 2) & 3][1], vval(A, lda, j0, nbp, i, 8 * fi + g),
+                vval(A, lda, j0, nbp, i, 8 * fj + g));
+    }
+    const bool oki = 8 * fi + g < nbp, okj = 8 * fj + g < nbp;
+    const double* ci = A + (j0 + 8 * fi + g) * lda;
+    const double* cj = A + (j0 + 8 * fj + g) * lda;
+    for (; k < kend; k += 16) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = k + 4 * u + t;
+        const bool in = k + 4 * u < kend;
+        av[u] = (in && oki) ? ci[i] : 0.0;
+        bv[u] = (in && okj) ? cj[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma8x8x4(c[u][0], c[u][1], av[u], bv[u]);
+    }
+    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+    G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + 1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
+  }
+}
+
+// T (dlarft forward/columnwise) from G = V^T V and tau, whole CTA:
+//   8x8 diagonal blocks by the column recurrence T(0:c, c) = -tau_c T(0:c,0:c) G(0:c, c)
+//   (four warps in parallel), then the block formula
+//   T = [[T1, -T1 G12 T2], [0, T2]]  for 8+8 -> 16 and 16+16 -> 32.
+template <int NTG>
+HBS_DEV void form_t(double* T, double* scratch, const double* G, const double* s_tau, int j0, int nbp) {
+  const int warp = (ltid<NTG>() >> 5), lane = ltid<NTG>() & 31;
+  for (int e = ltid<NTG>(); e < kP * kLdT; e += gthreads<NTG>()) T[e] = 0.0;
+  gsync<NTG>();
+  if (warp < 4 && lane < 8) {
+    const int base = 8 * warp, a = base + lane;
+    double trow[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cc = base + c;
+      const double tc = (cc < nbp) ? s_tau[j0 + cc] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < c; ++q)
+        if (q >= lane) acc = fma(trow[q], G[(base + q) * kLdT + cc], acc);
+      trow[c] = (lane < c) ? -tc * acc : (lane == c ? tc : 0.0);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) T[a * kLdT + base + c] = trow[c];
+  }
+  gsync<NTG>();
+  // combine: width 8 -> 16 (two pairs), then 16 -> 32
+  for (int w = 8; w < kP; w *= 2) {
+    const int npair = kP / (2 * w);
+    // X = G12 T2 for every pair  (w x w each)
+    for (int e = ltid<NTG>(); e < npair * w * w; e += gthreads<NTG>()) {
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = 0; q <= c; ++q) acc = fma(G[(o1 + i) * kLdT + o2 + q], T[(o2 + q) * kLdT + o2 + c], acc);
+      scratch[e] = acc;
+    }
+    gsync<NTG>();
+    // T12 = -T1 X
+    for (int e = ltid<NTG>(); e < npair * w * w; e += gthreads<NTG>()) {
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = i; q < w; ++q) acc = fma(T[(o1 + i) * kLdT + o1 + q], scratch[pr * w * w + q * w + c], acc);
+      T[(o1 + i) * kLdT + o2 + c] = -acc;
+    }
+    gsync<NTG>();
+  }
+}
+
+}  // namespace
+
+namespace {
+
+// inverse of the 32x32 upper-triangular block R(j0:j0+32, j0:j0+32) (in A)
+// into out (32 x kLdT) by the group: 8x8 diagonal blocks by lane-per-column
+// back substitution, then inv([[A,B],[0,C]]) = [[A^-1, -A^-1 B C^-1],[0, C^-1]].
+template <int NTG, int BAR>
+HBS_DEV void ysync() { asm volatile("bar.sync %0, %1;\n" ::"n"(BAR), "n"(NTG) : "memory"); }
+
+// Inverse of the 32x32 upper-triangular block R(j0:j0+32, j0:j0+32) (in A),
+// by the warp group starting at warp `wb` (NTG threads, named barrier BAR):
+// 8x8 diagonal blocks by lane-per-column back substitution, then
+// inv([[A,B],[0,C]]) = [[A^-1, -A^-1 B C^-1],[0, C^-1]] for 8+8 and 16+16.
+// out / scratch may live in global memory (row-major, ld 32 / 256 doubles).
+template <int NTG, int BAR>
+HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* out, double* scratch, int wb) {
+  const int tid = threadIdx.x - 32 * wb, warp = (tid >> 5), lane = tid & 31;
+  auto R = [&](int i, int c) -> double {
+    if (i >= nbp || c >= nbp) return i == c ? 1.0 : 0.0;
+    return A[(j0 + i) + (j0 + c) * lda];
+  };
+  for (int e = tid; e < kP * kP; e += NTG) out[e] = 0.0;
+  ysync<NTG, BAR>();
+  if (warp < 4 && lane < 8) {
+    const int base = 8 * warp, c = lane;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      x[i] = x[i] / R(base + i, base + i);
+#pragma unroll
+      for (int k = 0; k < i; ++k) x[k] = fma(-R(base + k, base + i), x[i], x[k]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[(base + i) * kP + base + c] = x[i];
+  }
+  __threadfence_block();
+  ysync<NTG, BAR>();
+  for (int w = 8; w < kP; w *= 2) {
+    const int npair = kP / (2 * w);
+    for (int e = tid; e < npair * w * w; e += NTG) {   // X = B C^-1
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = 0; q <= c; ++q) acc = fma(R(o1 + i, o2 + q), out[(o2 + q) * kP + o2 + c], acc);
+      scratch[e] = acc;
+    }
+    __threadfence_block();
+    ysync<NTG, BAR>();
+    for (int e = tid; e < npair * w * w; e += NTG) {   // -A^-1 X
+      const int pr = e / (w * w), rem = e % (w * w), i = rem / w, c = rem % w;
+      const int o1 = 2 * w * pr, o2 = o1 + w;
+      double acc = 0.0;
+      for (int q = i; q < w; ++q) acc = fma(out[(o1 + i) * kP + o1 + q], scratch[pr * w * w + q * w + c], acc);
+      out[(o1 + i) * kP + o2 + c] = -acc;
+    }
+    __threadfence_block();
+    ysync<NTG, BAR>();
+  }
+}
+
+}  // namespace
+
+// Panel factorisation by CholeskyQR + Householder reconstruction (Ballard et
+// al.), for the fused kernel's panel group (NTG threads, named barrier 1).
+// The panel block P = A(j0:m, j0:j0+32) (rows below the finished R):
+//   Gp = P^T P = R^T R (tensor cores; Cholesky, row-owned, one warp),
+//   Q1 = P R^{-1} (tensor cores, in place),
+//   Q1(0:32, :) - S = L U with s_j = -sign of the current pivot (one warp),
+//   L2 = Q1(32:, :) U^{-1} (tensor cores, in place),
+//   T = -U S L^{-T}, R_hh = S R.
+// In exact arithmetic these are the reflectors (and T, R) the column-by-column
+// Householder chain (dlarfg signs) produces -- Householder QR is unique for a
+// given sign rule -- so the panel leaves A / T exactly as panel_factor_r +
+// form_t would, without a 32-step reduction chain.  Returns false (group-
+// uniform) for panels the chain must factor: partial panels, a Cholesky
+// breakdown, or min R_ii < 1e-2 max R_ii (the Gram squares the panel's
+// condition number; the chain also carries the reference's sigma screen).
+template <int NTG>
+static __device__ __noinline__ bool panel_factor_gram(double* A, int lda, int m, int j0, int nbp, double* G, double* T,
+                                               double* scr, int* s_flag) {
+  if (nbp != kP) return false;
+  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mp = round_up(m, 8);
+  double* sg = scr;   // signs s_j
+  // 1. Gp = P^T P (32 x 32, row-major in G): 16 tiles of 8 x 8
+  for (int tile = warp; tile < 16; tile += nw) {
+    const int fi = tile >> 2, fj = tile & 3;
+    const double* ci = A + (j0 + 8 * fi + g) * lda + t;
+    const double* cj = A + (j0 + 8 * fj + g) * lda + t;
+    double c[4][2] = {};
+    for (int k = j0; k < mp; k += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + 4 * u < mp) dmma8x8x4(c[u][0], c[u][1], ci[k + 4 * u], cj[k + 4 * u]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + e] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
+  }
+  gsync<NTG>();
+  // 2. Cholesky (row i in lane i), R into G's upper triangle; R^{-1} into T
+  if (warp == 0) {
+    double c[kP];
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? G[lane * kLdT + k] : 0.0;
+    const double gmax = warp_max(G[lane * kLdT + lane]);
+    bool ok = gmax > 0.0 && gmax < 1e300;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const double d = __shfl_sync(0xffffffffu, c[j], j);
+      ok = ok && (d > 1e-4 * gmax);                  // R_jj >= 1e-2 max R_ii (approximately)
+      const double rs = rsqrt_nr(d);
+      if (lane == j) {
+#pragma unroll
+        for (int k = 0; k < kP; ++k)
+          if (k >= j) c[k] *= rs;
+      }
+      double rji = 0.0;
+#pragma unroll
+      for (int k = j + 1; k < kP; ++k) {
+        const double rk = __shfl_sync(0xffffffffu, c[k], j);
+        if (k == lane) rji = rk;
+        if (lane > j && k >= lane) c[k] = fma(-rji, rk, c[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+      if (k >= lane) G[lane * kLdT + k] = c[k];
+    __syncwarp();
+    // row lane of R^{-1}: x R = e_lane
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < kP; ++k) {
+      c[k] *= rcp_nr(G[k * kLdT + k]);
+#pragma unroll
+      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], G[k * kLdT + l], c[l]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) T[lane * kLdT + k] = c[k];
+    if (lane == 0) *s_flag = __all_sync(0xffffffffu, ok) ? 1 : 0;
+    else __all_sync(0xffffffffu, ok);
+  }
+  gsync<NTG>();
+  if (!*s_flag) return false;
+  // 3. Q1 = P R^{-1} in place, 8-row blocks per warp
+  for (int r0 = j0 + 8 * warp; r0 < mp; r0 += 8 * nw) {
+    double a[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
+    double acc[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
+  }
+  gsync<NTG>();
+  // 4. sign-chosen LU of the top 32 x 32 block (row lane in lane); U^{-1}
+  //    into T (R^{-1} is dead); R_hh = S R into A's upper triangle (U is dead
+  //    once U^{-1} and the T rows are formed); T = -U S L^{-T} rows into G
+  if (warp == 0) {
+    double c[kP];
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = A[(j0 + lane) + (j0 + k) * lda];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      double dinv = 0.0;
+      if (lane == j) {
+        const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
+        c[j] -= sj;
+        sg[j] = sj;
+        dinv = rcp_nr(c[j]);
+      }
+      dinv = __shfl_sync(0xffffffffu, dinv, j);
+      const double l = c[j] * dinv;
+      if (lane > j) c[j] = l;
+#pragma unroll
+      for (int k = j + 1; k < kP; ++k) {
+        const double uk = __shfl_sync(0xffffffffu, c[k], j);
+        if (lane > j) c[k] = fma(-l, uk, c[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) A[(j0 + lane) + (j0 + k) * lda] = c[k];
+    __syncwarp();
+    // column lane of U^{-1}: U z = e_lane, back substitution (c reused)
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = kP - 1; k >= 0; --k) {
+      c[k] *= rcp_nr(A[(j0 + k) + (j0 + k) * lda]);
+#pragma unroll
+      for (int q = 0; q < k; ++q) c[q] = fma(-A[(j0 + q) + (j0 + k) * lda], c[k], c[q]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP; ++k) T[k * kLdT + lane] = c[k];
+    // T row lane: -(U S) then forward substitution with L (unit lower)
+#pragma unroll
+    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? -A[(j0 + lane) + (j0 + k) * lda] * sg[k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+#pragma unroll
+      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], A[(j0 + l) + (j0 + k) * lda], c[l]);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kP; ++k)
+      if (k >= lane) A[(j0 + lane) + (j0 + k) * lda] = sg[lane] * G[lane * kLdT + k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kP; ++k) G[lane * kLdT + k] = c[k];
+  }
+  gsync<NTG>();
+  // 5. L2 = Q1(32:, :) U^{-1} in place
+  for (int r0 = j0 + kP + 8 * warp; r0 < mp; r0 += 8 * nw) {
+    double a[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
+    double acc[4][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
+  }
+  gsync<NTG>();
+  // 6. T from G
+  for (int e = ltid<NTG>(); e < kP * kP; e += gthreads<NTG>()) T[(e / kP) * kLdT + e % kP] = G[(e / kP) * kLdT + e % kP];
+  gsync<NTG>();
+  return true;
+}
+
+}  // namespace hbs

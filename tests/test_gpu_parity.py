@@ -161,6 +161,29 @@ def test_subtree_partition_on_one_gpu_bitwise(world):
         assert np.array_equal(d, f.discs[nid])
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_subtree_partition_bitwise_config4_shape(world):
+    """Same, at the config-4 box shape (128-row boxes, s = 192, r = 64), where
+    every (box, side) runs the persistent pipelined probe kernel: a box's bits
+    must not depend on how many boxes share its launch (one rank's level of 8
+    boxes vs the single-GPU level of 64)."""
+    import torch
+    from paper_2205_02990_b200 import synthetic
+    from paper_2205_02990_b200.distributed import compress_partitioned_on_one_device
+    n, leaf, k, s = 1 << 13, 128, 64, 192
+    tree = hb.build_tree(n, leaf)
+    gen = synthetic.device_generator(tree, k, seed=5, decay=0.9)
+    samples = tuple(m.cpu().numpy() for m in synthetic.device_samples(gen, s))
+    cfg = hb.CompressionConfig(rank=k, leaf_threshold=leaf)
+    f = hb.compress_from_samples(hb.SampleSet(*samples), tree, cfg)
+    blocks, root = compress_partitioned_on_one_device(samples, tree, cfg, world)
+    assert np.array_equal(root, f.root_disc)
+    for nid, (u, v, d) in blocks.items():
+        assert np.array_equal(u, f.u_bases[nid])
+        assert np.array_equal(v, f.v_bases[nid])
+        assert np.array_equal(d, f.discs[nid])
+
+
 @pytest.mark.parametrize("world", [1, 2, 4])
 def test_distributed_sampler_and_compressor_emulated(world):
     """Subtree-partitioned sampler (local up, level-lg exchange, replicated top,
