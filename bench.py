@@ -46,14 +46,22 @@ METRIC = "HBS compress-from-samples rows/s (fp64) at N=2^20,k=64"
 from paper_2205_02990_b200.roofline import PHASES, canonical_phase_flops, canonical_total_flops  # noqa: E402
 
 
-def fused_traffic():
-    """DRAM bytes per launch of the dominant (fused) kernel from the committed
-    ncu --set full capture (profiles/fused_traffic_r01.json), or None."""
+def fused_traffic(n_rows):
+    """DRAM bytes of the dominant (fused probe) kernel's leaf-level launch:
+    read + written bytes of the committed ncu --set full capture at N = 2^16
+    (profiles/fused_traffic_r02.json), scaled by rows to this run's leaf
+    launch (the kernel's traffic is linear in the number of boxes; the capture
+    shows it equal to the compulsory bytes).  Returns (bytes, note) or (None, None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "fused_traffic_r01.json")) as fh:
-            return float(json.load(fh)["traffic_bytes_per_launch"])
+        with open(os.path.join(ROOT, "profiles", "fused_traffic_r02.json")) as fh:
+            d = json.load(fh)
+        scale = n_rows / float(d["capture_n"])
+        return float(d["traffic_bytes_per_launch"]) * scale, (
+            f"leaf-level launch; ncu capture at N={d['capture_n']} ({d['traffic_bytes_per_launch']} B, "
+            f"{d['traffic_bytes_per_launch'] / d['algorithmic_bytes_per_launch']:.3f} x the algorithmic bytes) "
+            f"scaled x{scale:g} by rows")
     except (OSError, KeyError, ValueError):
-        return None
+        return None, None
 
 
 def fp64_peak():
@@ -226,7 +234,9 @@ def run_distributed(args, cfg, world, rank, dev):
     from paper_2205_02990_b200 import synthetic
     from paper_2205_02990_b200.distributed import DistributedCompressor, SubtreePartition
     N, k, leaf, s, r, decay = cfg
-    tree = hb.build_tree(N * world, leaf)
+    strong = args.scaling == "strong"
+    n_global = N if strong else N * world      # strong: the config's N split over the ranks
+    tree = hb.build_tree(n_global, leaf)
     part = SubtreePartition(tree, world, rank, r)
     t0 = time.perf_counter()
     op = synthetic.partitioned_generator(part, k, seed=0, decay=decay, device=dev)
@@ -259,7 +269,40 @@ def run_distributed(args, cfg, world, rank, dev):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dist.barrier()
     ms_step = float(t.item()) / args.steps
-    value = N * world / (ms_step / 1e3)
+    value = n_global / (ms_step / 1e3)
+    # end to end: this rank's rows from pinned host memory, compress, this rank's
+    # blocks (and the replicated top on rank 0) back to pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty(part.rows, s, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+        for h, dsrc in zip(host, (om, ps, y, z)):
+            h.copy_(dsrc)
+        dq = [torch.empty_like(om) for _ in range(4)]
+        outs = [m for lv, _, _ in part.local_specs for m in comp.local.levels[lv]]
+        if rank == 0 and comp.top is not None:
+            outs += [m for lv, _, _ in comp.top.specs for m in comp.top.levels[lv]] + [comp.top.root]
+        hout = [torch.empty(m.shape, dtype=m.dtype, pin_memory=True) for m in outs]
+        times = []
+        for it_ in range(args.e2e_steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for d_, h in zip(dq, host):
+                d_.copy_(h, non_blocking=True)
+            comp.run(*dq)
+            for h, m in zip(hout, outs):
+                h.copy_(m, non_blocking=True)
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t0], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if it_ > 0:
+                times.append(float(tt.item()))
+        nb = torch.tensor([4.0 * part.rows * s * 8, float(sum(m.numel() * 8 for m in outs))], device=dev)
+        dist.all_reduce(nb)
+        e2e = {"value": n_global / float(np.mean(times)), "unit": "rows/s", "h2d_bytes_per_step": int(nb[0].item()),
+               "d2h_bytes_per_step": int(nb[1].item()), "s_per_step": float(np.mean(times)),
+               "note": "sum over ranks of bytes; time = max over ranks (wall clock between barriers)"}
+        del host, dq, hout
     # accuracy through the distributed operators
     xg = torch.Generator(device=dev)
     xg.manual_seed(4 + rank)
@@ -274,13 +317,15 @@ def run_distributed(args, cfg, world, rank, dev):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox generator, seeded per rank)",
             "config": config_block(args, cfg, world),
             "roofline": {"bound": "fp64", "kernel": "whole sweep (all ranks)", "achieved": step_tf / world,
                          "peak": peak_tf, "unit": "TFLOP/s", "frac": step_tf / world / peak_tf, "traffic": None,
                          "peak_source": peak_src, "step_achieved_all_gpus": step_tf},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "cpu_baseline": None, "cpu_baseline_note": "timed on rank 0 at N = 1 only (bench contract)",
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),
             "accuracy": {"rel_apply_err_vs_truth": err, "probe": "x = N(0,1), 8 columns per rank"},
             "gen_seconds": t_gen,
         }
@@ -312,12 +357,16 @@ def make_workload(name, cfg, tree, dev, seed):
 
 def config_block(args, cfg, world):
     N, k, leaf, s, r, decay = cfg
+    strong = world > 1 and getattr(args, "scaling", "weak") == "strong"
+    per_gpu, total = (N // world, N) if strong else (N, N * world)
     what = ("ellipse log kernel (numerical rank), dense DMMA sampler" if args.config in KERNEL_CONFIGS
             else "exact-rank synthetic HBS, HBS sampler")
-    return {"workload": f"{args.config}: {what}, N={N} per GPU, k={k}, r={r}, leaf={leaf}, "
+    return {"workload": f"{args.config}: {what}, N={per_gpu} per GPU, k={k}, r={r}, leaf={leaf}, "
                         f"s={s}" + (f", coupling decay {decay}" if decay else ""),
-            "N_per_gpu": N, "k": k, "r": r, "leaf": leaf, "s": s, "global_rows": N * world,
+            "N_per_gpu": per_gpu, "k": k, "r": r, "leaf": leaf, "s": s, "global_rows": total,
             "parallelism": f"subtree x{world}" if world > 1 else "single GPU",
+            "launch": ("one CUDA-graph replay per sweep" if world == 1 and getattr(args, "graph", False)
+                       else "stream launches"),
             "l2_policy": "inputs (4 x N x s fp64) exceed L2 126 MB; no flush needed"}
 
 
@@ -333,8 +382,13 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 13)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = N rows per GPU (default), strong = the config's N split over the GPUs")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="replay the sweep from a CUDA graph (CompressPlan.run_graph; default)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     args = ap.parse_args()
     cfg = list(CONFIGS[args.config])
     if args.n:
@@ -387,13 +441,21 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     launches0 = lib.hbs_launch_counter()
+    graph_launches = 0
+    if args.graph:   # capture before the timed region
+        plan.run_graph(om, ps, y, z)
+        torch.cuda.synchronize()
+        launches0 = lib.hbs_launch_counter()
     with ClockSampler(local) as clocks:
         e0.record(stream)
         for _ in range(args.steps):
-            plan.run(om, ps, y, z)
+            if args.graph:
+                graph_launches += plan.run_graph(om, ps, y, z)
+            else:
+                plan.run(om, ps, y, z)
         e1.record(stream)
         torch.cuda.synchronize()
-    launches = (lib.hbs_launch_counter() - launches0)
+    launches = (lib.hbs_launch_counter() - launches0) + graph_launches
     ms_total = e0.elapsed_time(e1)
     ms_step = ms_total / args.steps
     value = N * world / (ms_step / 1e3)
@@ -421,6 +483,7 @@ def main():
         phase_ms["probe_qr_apply_q_fused"] = phase_ms.pop("probe_qr")
         phase_flops["probe_qr_apply_q_fused"] = phase_flops.pop("probe_qr")
     dom = max(phase_ms, key=lambda p: phase_ms[p])
+    traffic, traffic_src = fused_traffic(N) if (s, r, leaf) == (192, 64, 128) else (None, None)
     achieved = phase_flops[dom] / (phase_ms[dom] / 1e3) / 1e12
     total_flops = canonical_total_flops(tree, s, r)
     step_tf = total_flops / (ms_step / 1e3) / 1e12
@@ -458,7 +521,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox generator, seeded)",
             "config": config_block(args, cfg, world),
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": fused_traffic(), "peak_source": peak_src,
+                         "frac": achieved / peak_tf, "frac_of_spec_40tf": achieved / 40.0,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "step_achieved": step_tf, "step_frac": step_tf / peak_tf,
                          "step_canonical_flops": total_flops,
                          "phase_ms": phase_ms, "phase_tflops": {p: (phase_flops[p] / (phase_ms[p] / 1e3) / 1e12

@@ -276,6 +276,28 @@ class CompressPlan:
         if self.with_root:
             self.run_root(quad[0], quad[2], stream=st)
 
+    def run_graph(self, omega, psi, y, z):
+        """The same sweep replayed from a CUDA graph (captured on first use for
+        this quadruple's addresses, after one plain run that sets the kernels'
+        attributes): the ~230 launches of a sweep become one graph launch,
+        which removes the host launch gaps between the short kernels of the
+        upper levels.  Returns the number of kernels of this library in the
+        graph (the launches one replay performs)."""
+        key = tuple(m.data_ptr() for m in (omega, psi, y, z))
+        if getattr(self, "_graph_key", None) != key:
+            lib = _native.lib()
+            self.run(omega, psi, y, z)
+            torch.cuda.synchronize(self.device)
+            graph = torch.cuda.CUDAGraph()
+            n0 = lib.hbs_launch_counter()
+            with torch.cuda.graph(graph):
+                self.run(omega, psi, y, z)
+            self._graph, self._graph_key, self._graph_quad = graph, key, self.top_quad
+            self._graph_launches = int(lib.hbs_launch_counter() - n0)
+        self._graph.replay()
+        self.top_quad = self._graph_quad
+        return self._graph_launches
+
     def run_root(self, omega_root, y_root, stream=None):
         """Root core D_root = Y_root Omega_root^+ (compress.py:230-233)."""
         lib = _native.lib()

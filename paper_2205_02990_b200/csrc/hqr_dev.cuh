@@ -133,8 +133,20 @@ HBS_DEV int gthreads() { return NTG == 0 ? (int)blockDim.x : NTG; }
 // Logical thread index of a warp group.  In the fused kernel (NTG == 256) the
 // latency-critical panel group runs on physical warps 8..15, which the warp
 // arbiter favours (highest warp id first), so logical = physical ^ 256.
+#ifdef HBS_GROUPS_BY_SMSP
+// (fused_pipe.cu) the two warp groups live on disjoint SM sub-partitions: a
+// warp's sub-partition is warp % 4, group P = sub-partitions 0, 1 (logical
+// threads 0..255), group Y = sub-partitions 2, 3 (logical threads 256..511).
+template <int NTG>
+HBS_DEV int ltid() {
+  if (NTG != 256) return (int)threadIdx.x;
+  const int w = threadIdx.x >> 5;
+  return ((((w & 2) ? 8 : 0) + ((w >> 2) << 1) + (w & 1)) << 5) + (threadIdx.x & 31);
+}
+#else
 template <int NTG>
 HBS_DEV int ltid() { return NTG == 256 ? (int)(threadIdx.x ^ 256u) : (int)threadIdx.x; }
+#endif
 
 // A(j0:m, cb:ce) <- (I - V op(T) V^T) A(j0:m, cb:ce), V = panel j0 (nbp cols),
 // op(T) = T^T when trans (dgeqrf trailing update, H^T from the left), else T
@@ -1034,8 +1046,10 @@ HBS_DEV void ysync() { asm volatile("bar.sync %0, %1;\n" ::"n"(BAR), "n"(NTG) : 
 // inv([[A,B],[0,C]]) = [[A^-1, -A^-1 B C^-1],[0, C^-1]] for 8+8 and 16+16.
 // out / scratch may live in global memory (row-major, ld 32 / 256 doubles).
 template <int NTG, int BAR>
-HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* out, double* scratch, int wb) {
-  const int tid = threadIdx.x - 32 * wb, warp = (tid >> 5), lane = tid & 31;
+HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* out, double* scratch, int wb,
+                           int gtid = -1) {
+  // gtid: the caller's index within its group (default: physical warps wb .. wb + NTG/32 - 1)
+  const int tid = gtid >= 0 ? gtid : (int)threadIdx.x - 32 * wb, warp = (tid >> 5), lane = tid & 31;
   auto R = [&](int i, int c) -> double {
     if (i >= nbp || c >= nbp) return i == c ? 1.0 : 0.0;
     return A[(j0 + i) + (j0 + c) * lda];

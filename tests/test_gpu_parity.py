@@ -368,3 +368,30 @@ def test_chunked_levels_bitwise():
         for a, b in zip(full.levels[lvl], small.levels[lvl]):
             assert torch.equal(a, b)
     assert torch.equal(full.status, small.status)
+
+
+def test_graph_replay_equals_stream_launches():
+    """CompressPlan.run_graph (one CUDA-graph replay per sweep) leaves the same
+    bits as the plain launch sequence, for repeated replays."""
+    import torch
+    from paper_2205_02990_b200 import synthetic
+    n, leaf, k, s = 1 << 12, 128, 64, 192
+    tree = hb.build_tree(n, leaf)
+    gen = synthetic.device_generator(tree, k, seed=2, decay=0.9)
+    quad = synthetic.device_samples(gen, s)
+    plan = hb.CompressPlan(tree, s, k)
+    plan.run(*quad)
+    torch.cuda.synchronize()
+    want = [[m.clone() for m in plan.levels[lv]] for lv in sorted(plan.levels)] + [[plan.root.clone()]]
+    for m in (m for lv in plan.levels.values() for m in lv):
+        m.zero_()
+    plan.root.zero_()
+    for _ in range(2):
+        nk = plan.run_graph(*quad)
+    torch.cuda.synchronize()
+    plan.raise_for_status()
+    assert nk > 0
+    got = [[m for m in plan.levels[lv]] for lv in sorted(plan.levels)] + [[plan.root]]
+    for a, b in zip(want, got):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)

@@ -2,7 +2,7 @@
 import ctypes, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", ".."))
 import paper_2205_02990_b200._native as nat
-nat.LIB_PATH = os.path.join(os.path.dirname(__file__), "_hbs_b200_trace.so")
+nat.LIB_PATH = os.environ.get("HBS_B200_LIB") or os.path.join(os.path.dirname(__file__), "_hbs_b200_trace.so")
 import torch
 import paper_2205_02990_b200 as hb
 from paper_2205_02990_b200 import synthetic
