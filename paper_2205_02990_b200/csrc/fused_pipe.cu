@@ -7,8 +7,7 @@
 // compress_node_bases / compute_discrepancy, compress.py:155-197): group P
 // (warps 8..15) factors Omega_tau^T by the dlarfg Householder chain in shared
 // memory, group Y (warps 0..7) applies every finished panel to the box's Y rows
-// in tensor memory and solves X = (Y Q1) R^{-T}.  The results are bitwise
-// those of the one-shot kernel.
+// in tensor memory and solves X = (Y Q1) R^{-T}.
 //
 // What changes is the schedule, which is built around group P's reflector
 // chain being the critical resource (measured: ~45k cycles per panel alone,
