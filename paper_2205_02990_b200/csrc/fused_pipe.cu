@@ -30,6 +30,7 @@
 // 128-row box at s = 192 runs here, whatever the level size: a box's bits do
 // not depend on how many boxes share its launch (multi-GPU partitions stay
 // bitwise equal to the single-GPU sweep).
+#include <cstdlib>
 #include "hqr_dev.cuh"
 
 namespace hbs {
@@ -475,6 +476,9 @@ __global__ void __launch_bounds__(512, 1) probe_fused_pipe_kernel(FusedArgs args
 int launch_probe_fused_pipe(FusedArgs& args, int nsides, cudaStream_t stream) {
   constexpr int NF = 128, SF = 192;
   if (args.s != SF || args.n_max != NF || args.pre || args.gflag != nullptr) return 0;
+  // default: the SMSP-split form (fused_split.cu); HBS_SPLIT=0 keeps this kernel
+  static const bool use_split = [] { const char* e = std::getenv("HBS_SPLIT"); return !(e && e[0] == '0'); }();
+  if (use_split) return launch_probe_fused_split(args, nsides, stream);
   static const int n_sm = [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);

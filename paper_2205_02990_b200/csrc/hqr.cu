@@ -1143,7 +1143,9 @@ static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
     if (fused_tmem_ok(args) && args.s == 192 && args.n_max == 128) {
       // the persistent pipelined kernel (fused_pipe.cu; HBS_PIPE=0 keeps the one-shot kernel)
       static const bool use_pipe = [] { const char* e = std::getenv("HBS_PIPE"); return !(e && e[0] == '0'); }();
-      const int pr = use_pipe ? launch_probe_fused_pipe(args, nsides, stream) : 0;
+      static const bool use_split = [] { const char* e = std::getenv("HBS_SPLIT"); return e && e[0] == '1'; }();
+      const int pr = use_split ? launch_probe_fused_split(args, nsides, stream)
+                               : (use_pipe ? launch_probe_fused_pipe(args, nsides, stream) : 0);
       if (pr < 0) return kErrCuda;
       if (pr == 0) {
         const int rc = launch_fused_t<6, true, 128, 192>(args, nsides, stream);

@@ -98,6 +98,8 @@ int launch_probe_fused(FusedArgs args, int nsides, cudaStream_t stream);
 // Persistent pipelined form for config-4 shaped levels (fused_pipe.cu): 1 = ran on the
 // 128-row boxes, 0 = shape or size does not apply, < 0 = launch error.
 int launch_probe_fused_pipe(FusedArgs& args, int nsides, cudaStream_t stream);
+// Same with the two warp groups on disjoint SM sub-partitions (fused_split.cu; HBS_SPLIT=1).
+int launch_probe_fused_split(FusedArgs& args, int nsides, cudaStream_t stream);
 
 // ---------------------------------------------------------------- Gram probe factorisation
 // Per (box, side) with nullity s - n == r: Cholesky of Omega Omega^T and
