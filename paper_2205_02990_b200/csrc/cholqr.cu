@@ -21,6 +21,7 @@
 // condition number beyond about 1e6, a rank-deficient or zero block, or a
 // non-finite value) flags the (box, side); the caller then re-runs the
 // Householder kernel (hqr.cu, mode ortho) for the flagged blocks only.
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -513,7 +514,10 @@ static int launch_cholqr_t(const GeqrfArgs& args, int nsides, int32_t* flag, siz
 int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream) {
   const int nmax = args.m_max, r = args.n_fixed;
   if (!cholqr_fits(nmax, r)) return kErrUnsupported;
-  const size_t smem = cholqr_smem_bytes(nmax, r);
+  size_t smem = cholqr_smem_bytes(nmax, r);
+  // HBS_CQ_SOLO=1 (experiment): one CTA per SM instead of two
+  static const bool solo = [] { const char* e = std::getenv("HBS_CQ_SOLO"); return e && e[0] == '1'; }();
+  if (solo) smem = 120 * 1024;
   args.skip_rows = 0;
 #ifndef HBS_NO_CHOLQR_SPECIAL
   if (nmax == 128 && r == 64) {   // config-4 shape: compile-time loop bounds

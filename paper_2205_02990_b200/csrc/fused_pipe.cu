@@ -475,10 +475,11 @@ __global__ void __launch_bounds__(512, 1) probe_fused_pipe_kernel(FusedArgs args
 // does not apply, < 0 on a launch error.
 int launch_probe_fused_pipe(FusedArgs& args, int nsides, cudaStream_t stream) {
   constexpr int NF = 128, SF = 192;
-  if (args.s != SF || args.n_max != NF || args.pre || args.gflag != nullptr) return 0;
+  if (args.s != SF || args.pre || args.gflag != nullptr) return 0;
   // default: the SMSP-split form (fused_split.cu); HBS_SPLIT=0 keeps this kernel
   static const bool use_split = [] { const char* e = std::getenv("HBS_SPLIT"); return !(e && e[0] == '0'); }();
   if (use_split) return launch_probe_fused_split(args, nsides, stream);
+  if (args.n_max != NF) return 0;
   static const int n_sm = [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
@@ -491,6 +492,8 @@ int launch_probe_fused_pipe(FusedArgs& args, int nsides, cudaStream_t stream) {
   cudaFuncSetAttribute(probe_fused_pipe_kernel<NF, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   probe_fused_pipe_kernel<NF, SF><<<(unsigned)(total < n_sm ? total : n_sm), 512, smem, stream>>>(args, nsides);
   note_launch();
+  args.skip_rows = NF;
+  args.skip_rows_lo = NF - 1;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -11,6 +11,12 @@
 // Tensor memory is reachable per sub-partition only (lanes 32 (warp % 4) ..),
 // so group Y keeps box rows 64..127 in TMEM lanes 64..127 (four warps, 16 rows
 // each) and streams rows 0..63 through L2 (four warps, two 8-row groups each).
+//
+// Boxes with 97..128 rows (uneven trees) run here too, zero-padded to 128:
+// the missing columns of Omega^T are zero, so their reflectors are identities
+// (dlarfg: tau = 0 for a zero column) and leave the real reflectors, R and Y Q
+// untouched; the screen skips them, the R-block inverse treats their diagonal
+// as 1, and the missing Y rows are zero in TMEM and never written back.
 #define HBS_GROUPS_BY_SMSP
 #include "hqr_dev.cuh"
 
@@ -42,8 +48,9 @@ constexpr size_t split_smem_doubles() {
 // runs the back substitution x = e_c; for i = 31..0: x_i *= 1 / R_ii, x_k -= R_ki
 // x_i (k < i) -- the rinv_blocks_kernel recurrence (hqr.cu); R entries are
 // warp-uniform shared-memory reads.  out: 32 x 32 row-major.
-__device__ __noinline__ void tri_inverse32_warp(const double* A, int lda, int j0, double* out, int lane) {
-  const double dinv = 1.0 / A[(j0 + lane) + (size_t)(j0 + lane) * lda];   // lane i: 1 / R_ii (off the chain)
+__device__ __noinline__ void tri_inverse32_warp(const double* A, int lda, int j0, int nbp, double* out, int lane) {
+  // lane i: 1 / R_ii (off the chain); columns >= nbp are zero padding: identity
+  const double dinv = lane < nbp ? 1.0 / A[(j0 + lane) + (size_t)(j0 + lane) * lda] : 1.0;
   double x[kP];
 #pragma unroll
   for (int i = 0; i < kP; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
   // items of this CTA: w = blockIdx.x + k gridDim.x whose box has NF rows
   auto next_item = [&](int64_t w) -> int64_t {
     for (w += gridDim.x; w < total; w += gridDim.x)
-      if (box_rows(args.geo, w % nbox) == NF) break;
+      if (const int rows = box_rows(args.geo, w % nbox); rows > NF - kP && rows <= NF) break;
     return w;
   };
   int64_t w = (int64_t)blockIdx.x - (int64_t)gridDim.x;
@@ -119,10 +126,16 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
     // TMA bulk copies, one per Omega row (= column of Omega^T)
     auto load_cols = [&](int64_t item, int c0, int c1, uint64_t* bar) {
       const FusedSide& S = args.side[item / nbox];
-      const double* src = S.om + S.om_c_rb * args.geo.row_begin[item % nbox];
-      if (lt == 0) mbar_expect_tx(bar, (unsigned)((c1 - c0) * m * sizeof(double)));
+      const int64_t bi = item % nbox;
+      const double* src = S.om + S.om_c_rb * args.geo.row_begin[bi];
+      const int nb = box_rows(args.geo, bi);
+      const int ce = c1 < nb ? c1 : nb;              // real columns of the range
+      const int z0 = c0 > nb ? c0 : nb;              // pad columns [z0, c1): zero
+      for (int e = lt; e < (c1 - z0) * m; e += 256) A[(z0 + e / m) * lda + e % m] = 0.0;
+      __threadfence_block();
       gsync<256>();
-      for (int j = c0 + lt; j < c1; j += 256)
+      if (lt == 0) mbar_expect_tx(bar, (unsigned)((ce - c0) * m * sizeof(double)));
+      for (int j = c0 + lt; j < ce; j += 256)
         bulk_g2s(&A[j * lda], src + (int64_t)j * s, (unsigned)(m * sizeof(double)), bar);
     };
     unsigned nhh = 0;   // panels factored so far (step-barrier parity)
@@ -134,6 +147,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
       const FusedSide& S = args.side[w / nbox];
       double* tglob = S.t + (size_t)b * S.t_stride;
       double* rglob = S.rinv + (size_t)b * S.rinv_stride;
+      const int nb = box_rows(args.geo, b);
 #pragma unroll 1
       for (int p = 0; p < npanel; ++p) {
         const int j0 = p * kP;
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
       }
       if (lt < 32) {   // sigma screen on diag(R)
         double lo = INFINITY, hi = 0.0;
-        for (int j = lt; j < n; j += 32) {
+        for (int j = lt; j < nb; j += 32) {
           const double d = fabs(A[j + j * lda]);
           lo = fmin(lo, d);
           hi = fmax(hi, d);
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
         }
       }
       // R's diagonal-block inverses for group Y's solve (it is still applying the last panel)
-      if (lw < npanel) tri_inverse32_warp(A, lda, lw * kP, rglob + (size_t)lw * kP * kP, lane);
+      if (lw < npanel) tri_inverse32_warp(A, lda, lw * kP, nb - lw * kP, rglob + (size_t)lw * kP * kP, lane);
       __threadfence_block();
       gsync<256>();
       if (lt == 0) { mbar_arrive(s_rinv); PIPE_MARK(12); }
@@ -301,13 +315,15 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
     double* rglob = S.rinv + (size_t)b * S.rinv_stride;
     double* yq = S.yq + (size_t)b * S.yq_stride;
     const double* y0 = S.y + S.y_c_rb * rb;
+    const int nb = box_rows(args.geo, b);
+    const bool okh[2] = {rws[0] < nb, rws[1] < nb};   // (only TMEM rows can be missing: nb > 96)
     if (tmw) {
       for (int c0 = 0; c0 < scol; c0 += 16) {
         double v[4][2];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) v[q][h] = __ldcs(y0 + (size_t)rws[h] * s + c0 + 4 * q + t);
+          for (int h = 0; h < 2; ++h) v[q][h] = okh[h] ? __ldcs(y0 + (size_t)rws[h] * s + c0 + 4 * q + t) : 0.0;
         tm_st16(tl + 2 * c0, v);
       }
       tm_wait_st();
@@ -560,7 +576,8 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) yq[(size_t)rws[h] * s + c0 + 4 * q + t] = v[q][h];
+          for (int h = 0; h < 2; ++h)
+            if (okh[h]) yq[(size_t)rws[h] * s + c0 + 4 * q + t] = v[q][h];
       }
     }
     if (yw == 0 && lane == 0) PIPE_MARK(22);
@@ -576,7 +593,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
 // launch_probe_fused_pipe (1 = ran, 0 = shape does not apply, < 0 = error).
 int launch_probe_fused_split(FusedArgs& args, int nsides, cudaStream_t stream) {
   constexpr int NF = 128, SF = 192;
-  if (args.s != SF || args.n_max != NF || args.pre || args.gflag != nullptr) return 0;
+  if (args.s != SF || args.n_max > NF || args.n_max <= NF - kP || args.pre || args.gflag != nullptr) return 0;
   static const int n_sm = [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
@@ -589,6 +606,8 @@ int launch_probe_fused_split(FusedArgs& args, int nsides, cudaStream_t stream) {
   cudaFuncSetAttribute(probe_fused_split_kernel<NF, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   probe_fused_split_kernel<NF, SF><<<(unsigned)(total < n_sm ? total : n_sm), 512, smem, stream>>>(args, nsides);
   note_launch();
+  args.skip_rows = NF;
+  args.skip_rows_lo = NF - kP;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   const int64_t b = blockIdx.x;
   const FusedSide& S = args.side[side];
   const int nb_rt = box_rows(args.geo, b);
-  if (NF ? nb_rt != NF : nb_rt == args.skip_rows) return;   // the other launch owns this box
+  if (NF ? nb_rt != NF : (nb_rt > args.skip_rows_lo && nb_rt <= args.skip_rows)) return;   // the other launch owns this box
   if (args.gflag != nullptr && ((args.gflag[(int64_t)side * args.geo.nbox + b] != 0) == PRE)) return;
   const int nb = NF ? NF : nb_rt;
   const int m = SF ? SF : args.s, n = nb, s = SF ? SF : args.s;
@@ -1122,6 +1122,7 @@ static bool fused_tmem_ok(const FusedArgs& args) {
 template <int MR>
 static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
   args.skip_rows = -1;
+  args.skip_rows_lo = -1;
   if (args.pre) {   // Gram-factored boxes: Y side only (TMEM rows)
     if (!fused_tmem_ok(args)) return kErrUnsupported;
 #ifndef HBS_NO_FUSED_SPECIAL
@@ -1130,6 +1131,7 @@ static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
         const int rc = launch_fused_t<6, true, 128, 192, true>(args, nsides, stream);
         if (rc != kOk) return rc;
         args.skip_rows = 128;
+        args.skip_rows_lo = 127;
       }
     }
 #endif
@@ -1140,18 +1142,18 @@ static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
     // config-4 shape: boxes of exactly 128 rows with s = 192 run a specialised
     // kernel (compile-time loop bounds); any other boxes of the level follow
     // in the generic kernel
-    if (fused_tmem_ok(args) && args.s == 192 && args.n_max == 128) {
-      // the persistent pipelined kernel (fused_pipe.cu; HBS_PIPE=0 keeps the one-shot kernel)
+    if (fused_tmem_ok(args) && args.s == 192 && args.n_max > 96 && args.n_max <= 128) {
+      // the persistent pipelined kernels (fused_pipe.cu / fused_split.cu; HBS_PIPE=0 keeps the
+      // one-shot kernel); they set the row range they covered in args.skip_rows(_lo)
       static const bool use_pipe = [] { const char* e = std::getenv("HBS_PIPE"); return !(e && e[0] == '0'); }();
-      static const bool use_split = [] { const char* e = std::getenv("HBS_SPLIT"); return e && e[0] == '1'; }();
-      const int pr = use_split ? launch_probe_fused_split(args, nsides, stream)
-                               : (use_pipe ? launch_probe_fused_pipe(args, nsides, stream) : 0);
+      const int pr = use_pipe ? launch_probe_fused_pipe(args, nsides, stream) : 0;
       if (pr < 0) return kErrCuda;
-      if (pr == 0) {
+      if (pr == 0 && args.n_max == 128) {
         const int rc = launch_fused_t<6, true, 128, 192>(args, nsides, stream);
         if (rc != kOk) return rc;
+        args.skip_rows = 128;
+        args.skip_rows_lo = 127;
       }
-      args.skip_rows = 128;
     }
   }
 #endif

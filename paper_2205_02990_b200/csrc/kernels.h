@@ -89,7 +89,8 @@ struct FusedArgs {
   FusedSide side[2];
   int s, n_max, lda;
   double tol;
-  int skip_rows;   // generic kernel: boxes with this many rows were done by a specialised launch (-1: none)
+  int skip_rows;   // generic kernel: boxes with skip_rows_lo < rows <= skip_rows were done by a specialised launch (-1: none)
+  int skip_rows_lo;
   int pre;                  // 1: apply the Gram factorisation (fac) instead of factoring Omega
   const int32_t* gflag;     // Gram flags (side*nbox + b): PRE takes flag 0, Householder flag != 0
 };
