@@ -139,6 +139,15 @@ int hbs_basis_orth(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off
 /* Number of CUDA kernels launched by this library so far (process-wide). */
 unsigned long long hbs_launch_counter(void);
 
+/* Optional hint for the NEXT hbs_compress_level / hbs_compress_level_profiled
+ * call of the calling thread: the smallest box of the level has `min_rows`
+ * rows (the host knows the tree, tree.py:63-102; the library only sees device
+ * pointers).  When min_rows == max_rows every box has the shape the
+ * specialised kernels cover, and the generic launches that would find no box
+ * are skipped.  Results do not depend on the hint; 0 (the default after every
+ * level call) means unknown. */
+void hbs_level_hint(int min_rows);
+
 /* Root core D_root = Y_root Omega_root^+ (compress.py:230-233), rows = 2r.
  * `row_begin`/`sq_off` describe the single root box ({0, 2r} / {0, 4r^2}). */
 int hbs_root_workspace_bytes(int rows, int s, size_t* bytes);

@@ -36,6 +36,7 @@ SIGNATURES = {
     "hbs_compress_level_profiled": ([_I64, _P, _P, _I, _I, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                      _P, _P, _SZ, _P, _P, ctypes.POINTER(ctypes.c_float)], _I),
     "hbs_launch_counter": ([], ctypes.c_ulonglong),
+    "hbs_level_hint": ([ctypes.c_int], None),
     "hbs_probe_qr_scratch_bytes": ([_I64, _I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_basis_qr_scratch_bytes": ([_I64, _I, _I, ctypes.POINTER(_SZ)], _I),
     "hbs_basis_qr": ([_I64, _P, _P, _I, _I, _P, _P, _P, _P], _I),

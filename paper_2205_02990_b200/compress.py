@@ -217,6 +217,7 @@ class CompressPlan:
             geo, row0, sq0 = chunk_geo, int(g.begins_host[b0] - g.begins_host[0]), int(g.sq_host[b0])
             stat = status
         q = [m[row0:] for m in quad]
+        lib.hbs_level_hint(geo.min_rows)
         rc = lib.hbs_compress_level(
             geo.nbox, geo.row_begin.data_ptr(), geo.sq_off.data_ptr(), geo.max_rows, s, r, self.tol,
             q[0].data_ptr(), q[1].data_ptr(), q[2].data_ptr(), q[3].data_ptr(),
@@ -243,6 +244,7 @@ class CompressPlan:
         for b0, b1, geo, stat in parts:
             row0, sq0 = int(g.begins_host[b0] - g.begins_host[0]), int(g.sq_host[b0])
             q = [m[row0:] for m in quad]
+            lib.hbs_level_hint(geo.min_rows)
             rc = lib.hbs_compress_level_profiled(
                 geo.nbox, geo.row_begin.data_ptr(), geo.sq_off.data_ptr(), geo.max_rows, s, r, self.tol,
                 *(m.data_ptr() for m in q), u[row0:].data_ptr(), v[row0:].data_ptr(), d[sq0:].data_ptr(),

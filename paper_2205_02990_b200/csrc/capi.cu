@@ -143,6 +143,10 @@ int gemm(const LevelGeo& geo, BDim M, BDim N, BDim K, int mmax, int nmax, BOpera
 
 #define HBS_TRY(x) do { int _e = (x); if (_e != kOk) return _e; } while (0)
 
+// hbs_level_hint: smallest box of the next level call (0 = unknown), consumed by that call
+thread_local int g_min_rows_hint = 0;
+thread_local int g_level_uniform = 0;   // the running level call: min rows == max rows
+
 // Probe factorisation + apply/solve for both sides of a level (or side 0 only).
 int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int nsides,
                      const double* om0, const double* om1, const double* y0, const double* y1,
@@ -152,6 +156,7 @@ int factor_and_solve(const LevelGeo& geo, int nr, int s, int r, double tol, int 
     FusedArgs f;
     std::memset(&f, 0, sizeof(f));
     f.geo = geo; f.s = s; f.n_max = nr; f.tol = tol;
+    f.uniform = g_level_uniform;
     const double* oms[2] = {om0, om1};
     const double* ys[2] = {y0, y1};
     for (int sd = 0; sd < nsides; ++sd) {
@@ -267,6 +272,8 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
                        const double* z, double* u, double* v, double* d, double* lift_omega,
                        double* lift_psi, double* lift_y, double* lift_z, void* workspace,
                        size_t workspace_bytes, int32_t* status, void* stream) {
+  g_level_uniform = (g_min_rows_hint == max_rows) ? 1 : 0;   // hbs_level_hint, consumed here
+  g_min_rows_hint = 0;
   if (nbox < 1 || max_rows < 1 || s < 1 || r < 1 || max_rows < r) return HBS_ERR_DIMENSION;
   if (s - max_rows < r) return HBS_ERR_CONFIGURATION;
   if (s > 512) return HBS_ERR_UNSUPPORTED;
@@ -298,6 +305,7 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   // of its complete Householder Q, linalg.py:52-62) is rotation-invariant
   // exactly when its nullity s - 2r equals r.  Every BASELINE config has
   // s = 3r; otherwise keep LAPACK's reflector-defined bases.
+  g.uniform = g_level_uniform;
   if (cholqr_fits(nr, r) && s <= 3 * r) {
     HBS_TRY(launch_cholqr(g, 2, w.qr_flag, st));
     g.only = w.qr_flag;
@@ -352,6 +360,8 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
 }
 
 unsigned long long hbs_launch_counter(void) { return g_launches.load(); }
+
+void hbs_level_hint(int min_rows) { g_min_rows_hint = min_rows; }
 
 int hbs_compress_level_profiled(int64_t nbox, const int64_t* row_begin, const int64_t* sq_off, int max_rows,
                                 int s, int r, double tol, const double* omega, const double* psi,
@@ -466,6 +476,8 @@ int hbs_root_workspace_bytes(int rows, int s, size_t* bytes) {
 int hbs_compress_root(const int64_t* row_begin, const int64_t* sq_off, int rows, int s, double tol,
                       const double* omega, const double* y, double* root, void* workspace,
                       size_t workspace_bytes, int32_t* status, void* stream) {
+  g_level_uniform = 0;   // (a level hint never applies to the root call)
+  g_min_rows_hint = 0;
   if (rows < 1 || s < rows) return HBS_ERR_DIMENSION;
   if (s > 512) return HBS_ERR_UNSUPPORTED;
   Carver c{static_cast<char*>(workspace)};

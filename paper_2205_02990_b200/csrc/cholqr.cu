@@ -526,6 +526,7 @@ int launch_cholqr(GeqrfArgs args, int nsides, int32_t* flag, cudaStream_t stream
     args.skip_rows = 128;
   }
 #endif
+  if (args.uniform && args.skip_rows == nmax) return kOk;   // every box went to the specialised launch
   return launch_cholqr_t<0, 0>(args, nsides, flag, smem, stream);
 }
 

@@ -67,7 +67,8 @@ __device__ __noinline__ void tri_inverse32_warp(const double* A, int lda, int j0
 
 }  // namespace
 
-template <int NF, int SF>
+// PAD = false: boxes of exactly NF rows; PAD = true: boxes of NF-31 .. NF-1 rows (zero-padded).
+template <int NF, int SF, bool PAD>
 __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs args, int nsides) {
   static_assert(NF == 128 && SF % 32 == 0 && SF <= 192, "shape");
   extern __shared__ __align__(16) double smem[];
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
   // items of this CTA: w = blockIdx.x + k gridDim.x whose box has NF rows
   auto next_item = [&](int64_t w) -> int64_t {
     for (w += gridDim.x; w < total; w += gridDim.x)
-      if (const int rows = box_rows(args.geo, w % nbox); rows > NF - kP && rows <= NF) break;
+      if (const int rows = box_rows(args.geo, w % nbox); PAD ? (rows > NF - kP && rows < NF) : rows == NF) break;
     return w;
   };
   int64_t w = (int64_t)blockIdx.x - (int64_t)gridDim.x;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
       const FusedSide& S = args.side[item / nbox];
       const int64_t bi = item % nbox;
       const double* src = S.om + S.om_c_rb * args.geo.row_begin[bi];
-      const int nb = box_rows(args.geo, bi);
+      const int nb = PAD ? box_rows(args.geo, bi) : NF;
       const int ce = c1 < nb ? c1 : nb;              // real columns of the range
       const int z0 = c0 > nb ? c0 : nb;              // pad columns [z0, c1): zero
       for (int e = lt; e < (c1 - z0) * m; e += 256) A[(z0 + e / m) * lda + e % m] = 0.0;
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
       const FusedSide& S = args.side[w / nbox];
       double* tglob = S.t + (size_t)b * S.t_stride;
       double* rglob = S.rinv + (size_t)b * S.rinv_stride;
-      const int nb = box_rows(args.geo, b);
+      const int nb = PAD ? box_rows(args.geo, b) : NF;
 #pragma unroll 1
       for (int p = 0; p < npanel; ++p) {
         const int j0 = p * kP;
@@ -315,8 +316,8 @@ __global__ void __launch_bounds__(512, 1) probe_fused_split_kernel(FusedArgs arg
     double* rglob = S.rinv + (size_t)b * S.rinv_stride;
     double* yq = S.yq + (size_t)b * S.yq_stride;
     const double* y0 = S.y + S.y_c_rb * rb;
-    const int nb = box_rows(args.geo, b);
-    const bool okh[2] = {rws[0] < nb, rws[1] < nb};   // (only TMEM rows can be missing: nb > 96)
+    const int nb = PAD ? box_rows(args.geo, b) : NF;
+    const bool okh[2] = {!PAD || rws[0] < nb, !PAD || rws[1] < nb};   // (only TMEM rows can be missing: nb > 96)
     if (tmw) {
       for (int c0 = 0; c0 < scol; c0 += 16) {
         double v[4][2];
@@ -603,9 +604,18 @@ int launch_probe_fused_split(FusedArgs& args, int nsides, cudaStream_t stream) {
   const int64_t total = args.geo.nbox * nsides;
   constexpr size_t smem = split_smem_doubles<NF, SF>() * sizeof(double);
   static_assert(smem <= kMaxSmemBytes, "shared memory");
-  cudaFuncSetAttribute(probe_fused_split_kernel<NF, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  probe_fused_split_kernel<NF, SF><<<(unsigned)(total < n_sm ? total : n_sm), 512, smem, stream>>>(args, nsides);
+  const unsigned grid = (unsigned)(total < n_sm ? total : n_sm);
+  if (args.n_max == NF) {   // the full boxes (every box of a perfect tree)
+    cudaFuncSetAttribute(probe_fused_split_kernel<NF, SF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    probe_fused_split_kernel<NF, SF, false><<<grid, 512, smem, stream>>>(args, nsides);
+    note_launch();
+  }
+  // boxes of NF-31 .. NF-1 rows (uneven trees; every CTA exits at once when there are none)
+  if (!(args.uniform && args.n_max == NF)) {
+  cudaFuncSetAttribute(probe_fused_split_kernel<NF, SF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_fused_split_kernel<NF, SF, true><<<grid, 512, smem, stream>>>(args, nsides);
   note_launch();
+  }
   args.skip_rows = NF;
   args.skip_rows_lo = NF - kP;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;

@@ -1157,6 +1157,8 @@ static int launch_fused_mr(FusedArgs& args, int nsides, cudaStream_t stream) {
     }
   }
 #endif
+  // every box has n_max rows and a specialised launch took that shape: the generic launch would find no box
+  if (args.uniform && args.n_max > args.skip_rows_lo && args.n_max <= args.skip_rows) return kOk;
   return fused_tmem_ok(args) ? launch_fused_t<MR, true>(args, nsides, stream)
                              : launch_fused_t<MR, false>(args, nsides, stream);
 }

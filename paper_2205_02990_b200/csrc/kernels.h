@@ -54,6 +54,7 @@ struct GeqrfArgs {
   int use_smem;
   const int32_t* only;  // if set: process (box b, side) only when only[side*nbox + b] != 0
   int skip_rows;        // cholqr generic kernel: boxes with this many rows went to a specialised launch (0: none)
+  int uniform;          // every box of the level has m_max rows (host hint)
 };
 
 // Blocked Householder (hqr.cu): kFactor also emits the per-panel T and R
@@ -91,6 +92,7 @@ struct FusedArgs {
   double tol;
   int skip_rows;   // generic kernel: boxes with skip_rows_lo < rows <= skip_rows were done by a specialised launch (-1: none)
   int skip_rows_lo;
+  int uniform;     // every box of the level has n_max rows (host hint): generic launches with no box are skipped
   int pre;                  // 1: apply the Gram factorisation (fac) instead of factoring Omega
   const int32_t* gflag;     // Gram flags (side*nbox + b): PRE takes flag 0, Householder flag != 0
 };

@@ -34,6 +34,7 @@ class LevelGeometry:
         sizes = np.diff(begins)
         self.nbox = sizes.size
         self.max_rows = int(sizes.max())
+        self.min_rows = int(sizes.min())
         self.total_rows = int(begins[-1] - begins[0])
         sq = np.zeros(self.nbox + 1, dtype=np.int64)
         np.cumsum(sizes * sizes, out=sq[1:])

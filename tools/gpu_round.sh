@@ -8,6 +8,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 KF='regex:probe_fused|hqr_kernel|bgemm|cholqr|rinv_blocks|applyq|fill_log|gram'
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KF" --csv --log-file gpurun_out/launches.csv python tools/profile_level.py --n 65536 --reps 1 > gpurun_out/ncu_launch.log 2>&1
 python tools/dbg/ll_sum.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:probe_fused_pipe -c 1 -o gpurun_out/fused python tools/profile_level.py --n 65536 --reps 1 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:probe_fused_split -c 1 -o gpurun_out/fused python tools/profile_level.py --n 65536 --reps 1 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cholqr -c 1 -o gpurun_out/cholqr python tools/profile_level.py --n 65536 --reps 1 >> gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgemm -s 20 -c 1 -o gpurun_out/bgemm python tools/profile_level.py --n 65536 --reps 1 >> gpurun_out/ncu_full.log 2>&1
