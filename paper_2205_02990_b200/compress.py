@@ -14,6 +14,7 @@ its node id and level (compress.py:260-265, 274-279).
 
 import ctypes
 import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -132,7 +133,8 @@ class CompressPlan:
     the lifted quadruple of the last compressed level (the multi-GPU hand-off)."""
 
     def __init__(self, tree: ClusterTree, s: int, rank: int, tol: float = DEFAULT_ILL_CONDITIONING_TOL,
-                 device=None, specs=None, with_root=None, out_levels=None, max_workspace_bytes=None):
+                 device=None, specs=None, with_root=None, out_levels=None, max_workspace_bytes=None,
+                 parent_geometry=None):
         self.tree, self.s, self.rank, self.tol = tree, s, rank, tol
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         r = rank
@@ -150,7 +152,9 @@ class CompressPlan:
         self.chunks = {}
         ws, lift_rows = 0, []
         for level, begins, first in self.specs:
-            g = LevelGeometry(begins, dev)
+            # (parent_geometry: whole-level geometries already on the device; slice them there)
+            g = (LevelGeometry.slice_of(parent_geometry[level], first, len(begins) - 1)
+                 if parent_geometry is not None and level in parent_geometry else LevelGeometry(begins, dev))
             self.geometry[level], self.first_box[level] = g, first
             if out_levels is not None and level in out_levels:   # caller-owned (views of full levels)
                 self.levels[level] = out_levels[level]
@@ -177,7 +181,8 @@ class CompressPlan:
                 self.chunks[level] = parts
             ws = max(ws, sz.value)
             lift_rows.append(g.nbox * r)
-        self.geometry[0] = LevelGeometry(np.array([0, 2 * r], dtype=np.int64), dev)
+        if self.with_root:   # (one small upload; the host pipeline's subtree plans have no root)
+            self.geometry[0] = LevelGeometry(np.array([0, 2 * r], dtype=np.int64), dev)
         sz = _size_t()
         _native.check(lib.hbs_root_workspace_bytes(2 * r, s, ctypes.byref(sz)), "workspace")
         ws = max(ws, sz.value)
@@ -448,8 +453,9 @@ def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, 
     n, s = host[0].shape
     r, tol = config.rank, config.ill_conditioning_tol
     L = tree.depth
+    _t = [time.perf_counter()] if os.environ.get("HBS_HOST_TIMING") else None
     if chunks is None:
-        chunks = int(os.environ.get("HBS_HOST_CHUNKS", "8"))
+        chunks = int(os.environ.get("HBS_HOST_CHUNKS", "16"))
     world = 1
     while world * 2 <= chunks and (world * 2).bit_length() - 1 < L:
         world *= 2
@@ -491,12 +497,14 @@ def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, 
     # every plan (buffers, geometry uploads) is built before any compute is
     # enqueued, so the launches of consecutive subtrees go out back to back
     plans = [CompressPlan(tree, s, r, tol, dev, specs=p.local_specs, with_root=(world == 1),
-                          out_levels=out_views(p.local_specs)) for p in parts]
+                          out_levels=out_views(p.local_specs), parent_geometry=geo) for p in parts]
     tspecs = parts[0].top_specs
     top = plans[0] if world == 1 else CompressPlan(tree, s, r, tol, dev, specs=tspecs, with_root=True,
-                                                   out_levels=out_views(tspecs))
+                                                   out_levels=out_views(tspecs), parent_geometry=geo)
     # (uploads after the plans: their small geometry copies must not queue
     # behind gigabytes of H2D on the copy engine)
+    if _t is not None:
+        _t.append(time.perf_counter())
     arrived = []
     for p in parts:              # all uploads back to back on the H2D stream
         with torch.cuda.stream(h2d):
@@ -519,7 +527,12 @@ def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, 
         else:
             top.run_root(top_quad[0], top_quad[2], stream=comp.cuda_stream)
         plans = plans + [top]
+    if _t is not None:
+        _t.append(time.perf_counter())
     torch.cuda.synchronize(dev)
+    if _t is not None:
+        _t.append(time.perf_counter())
+        print("host pipeline: plans built %.1f ms, enqueued %.1f ms, device done %.1f ms" % tuple(1e3 * (x - _t[0]) for x in _t[1:]), flush=True)
     fails = [f for f in (pl.first_failure() for pl in plans) if f is not None]
     if fails:
         level, nid = min(fails, key=lambda f: (-f[0], f[1]))

@@ -44,6 +44,26 @@ class LevelGeometry:
         self.row_begin = torch.from_numpy(begins - begins[0]).to(device)
         self.sq_off = torch.from_numpy(sq).to(device)
 
+    @classmethod
+    def slice_of(cls, parent: "LevelGeometry", first: int, nbox: int) -> "LevelGeometry":
+        """Geometry of boxes [first, first + nbox) of `parent`, with the device
+        arrays derived from the parent's on the device (two tiny kernels on
+        the current stream, no host-to-device copy: the host pipeline builds
+        one of these per subtree and level while gigabytes of samples are in
+        flight on the copy engine)."""
+        g = cls.__new__(cls)
+        begins = parent.begins_host[first:first + nbox + 1]
+        sizes = np.diff(begins)
+        g.nbox = nbox
+        g.max_rows, g.min_rows = int(sizes.max()), int(sizes.min())
+        g.total_rows = int(begins[-1] - begins[0])
+        g.begins_host = begins
+        g.sq_host = parent.sq_host[first:first + nbox + 1] - parent.sq_host[first]
+        g.sq_total = int(g.sq_host[-1])
+        g.row_begin = parent.row_begin[first:first + nbox + 1] - parent.row_begin[first:first + 1]
+        g.sq_off = parent.sq_off[first:first + nbox + 1] - parent.sq_off[first:first + 1]
+        return g
+
 
 def tree_geometry(tree: ClusterTree, rank: int, device):
     """Geometry of levels 0..L: the leaf level uses the tree's ranges, coarser
