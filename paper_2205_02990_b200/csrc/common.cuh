@@ -159,6 +159,21 @@ HBS_DEV void tm_alloc512(uint32_t* slot) {
       static_cast<unsigned>(__cvta_generic_to_shared(slot))));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
 }
+// Runtime column count (a power of two in 32 .. 512): a CTA that needs fewer
+// than 512 columns leaves the rest to the other CTAs resident on its SM.
+HBS_DEV void tm_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+      static_cast<unsigned>(__cvta_generic_to_shared(slot))), "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+HBS_DEV void tm_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols));
+}
+HBS_DEV uint32_t tm_pow2_cols(int need) {
+  uint32_t c = 32;
+  while ((int)c < need) c <<= 1;
+  return c;
+}
 HBS_DEV void tm_dealloc512(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
 }

@@ -368,7 +368,14 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
                     ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   if (threadIdx.x < kP + 34) mbar_init(&s_bar[threadIdx.x], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  if (TM && warp == 0) tm_alloc512(s_tmem);
+  // TMEM columns of this CTA: the Y rows (2 b32 columns per fp64 column) up to the
+  // solve's padded width; small boxes leave room for the other CTAs of the SM
+#ifdef HBS_PRE_PAIRS
+  const uint32_t tcols = 512;
+#else
+  const uint32_t tcols = TM ? tm_pow2_cols(2 * min(256, max(round_up(s, 16), round_up(n, 32) + 16))) : 0;
+#endif
+  if (TM && warp == 0) tm_alloc(s_tmem, tcols);
   tm_fence_before();
   __syncthreads();
   tm_fence_after();
@@ -676,7 +683,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       tm_fence_before();
       __syncthreads();
       tm_fence_after();
-      if (warp == 0) tm_dealloc512(tbase);
+      if (warp == 0) tm_dealloc(tbase, tcols);
       return;
     }
   }
@@ -956,7 +963,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     tm_fence_before();
     ysync<256, 2>();
     tm_fence_after();
-    if (yw == 0) tm_dealloc512(tbase);
+    if (yw == 0) tm_dealloc(tbase, tcols);
     if (yw == 0 && lane == 0) FUSED_MARK(41);
     return;
   }
