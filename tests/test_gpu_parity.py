@@ -222,6 +222,22 @@ def test_distributed_sampler_and_compressor_emulated(world):
             got = torch.cat([op.down_local(x[p.begin:p.end].contiguous(), q, ulg[p.rank * k:(p.rank + 1) * k], transpose)
                              for p, op, q in zip(parts, ops, qh)])
         assert float(torch.linalg.norm(got - want) / torch.linalg.norm(want)) <= 1e-14
+    # ... and compressing samples of that operator with the same partition
+    # (per-rank subtrees, concatenated level-lg lifts, replicated top) gives a
+    # factorization that reproduces it (oversampled: r = k + 8, s = 3r)
+    from paper_2205_02990_b200.distributed import compress_partitioned_on_one_device
+    om, ps = O.gaussian(n, s, 11, 0), O.gaussian(n, s, 11, 1)
+    y = hb.apply_matrix(full, om)
+    z = hb.apply_matrix(full, ps, transpose=True)
+    cfg = hb.CompressionConfig(rank=r, leaf_threshold=leaf)
+    blocks, root = compress_partitioned_on_one_device((om, ps, y, z), tree, cfg, world)
+    fc = hb.HbsFactorization(tree, r, {i: b[0] for i, b in blocks.items()}, {i: b[1] for i, b in blocks.items()},
+                             {i: b[2] for i, b in blocks.items()}, root)
+    xs = x.cpu().numpy()
+    for transpose in (False, True):
+        want = hb.apply_matrix(full, xs, transpose=transpose)
+        got = hb.apply_matrix(fc, xs, transpose=transpose)
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
 
 
 def test_power_method_relnorm_device():
@@ -398,3 +414,32 @@ def test_graph_replay_equals_stream_launches():
     for a, b in zip(want, got):
         for x, y in zip(a, b):
             assert torch.equal(x, y)
+
+
+def test_sigma_screen_window_is_one_sided():
+    """The documented difference of the ill-conditioning screen (DESIGN.md
+    section 6): the reference tests sigma_min / sigma_max of the probe block
+    (linalg.py:73-78), the GPU path min|R_ii| / max|R_ii| of its QR factor,
+    which is an upper bound of that ratio -- so it never raises where the
+    reference would not.  A Kahan block (|R_ii| = s^i, far smaller sigma_min)
+    sits in the window between the two: with a tolerance inside the window the
+    oracle rejects the block and the GPU stage accepts it; with the tolerance
+    above the diag(R) ratio both reject it."""
+    rows, cols = 32, 48
+    c, sn = 0.5, np.sqrt(0.75)
+    kahan = np.diag(sn ** np.arange(rows)) @ (np.eye(rows) - c * np.triu(np.ones((rows, rows)), 1))
+    m = np.zeros((rows, cols))
+    m[:, :rows] = kahan.T                                  # M^T = [K; 0]: R = K up to signs
+    b = O.gaussian(8, cols, 2, 0)
+    sv = np.linalg.svd(kahan, compute_uv=False)
+    diag_ratio, sigma_ratio = sn ** (rows - 1), sv[-1] / sv[0]
+    assert sigma_ratio < 1e-3 * diag_ratio                 # a real window
+    tol = float(np.sqrt(diag_ratio * sigma_ratio))         # sigma ratio < tol < diag(R) ratio
+    x, ratio = O.right_solve(b, m, tol)
+    assert x is None and ratio < tol                       # the reference's test rejects the block
+    got = hb.lstsq_right(b, m, tol)                        # inside the window: accepted (documented)
+    assert np.all(np.isfinite(np.asarray(got)))
+    with pytest.raises(hb.IllConditionedProbeError):
+        hb.lstsq_right(b, m, 2.0 * diag_ratio)
+    x, _ = O.right_solve(b, m, 2.0 * diag_ratio)
+    assert x is None
