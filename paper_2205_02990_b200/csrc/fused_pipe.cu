@@ -24,6 +24,9 @@
 //    range split over warp pairs, starting on the published reflectors
 //    (s_pub) while group P still forms T; group Y also inverts every diagonal
 //    block of R.
+// (This kernel shares every SM sub-partition between the two groups; the
+// default since round 2 is its SMSP-split successor, fused_split.cu, which
+// launch_probe_fused_pipe dispatches to unless HBS_SPLIT=0.)
 // All hand-offs are mbarriers whose phase parity is the item counter.  The
 // look-ahead's split K sum (rows [j0, mid) + rows [mid, m), in that order)
 // is the one difference in rounding from the one-shot kernel, so every

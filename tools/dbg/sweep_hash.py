@@ -10,7 +10,7 @@ tree = hb.build_tree(n, 128)
 gen = synthetic.device_generator(tree, 64, seed=0, decay=0.9)
 om, ps, y, z = synthetic.device_samples(gen, 192)
 plan = hb.CompressPlan(tree, 192, 64)
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", 2))):
     plan.run(om, ps, y, z)
     torch.cuda.synchronize()
     plan.raise_for_status()
