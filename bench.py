@@ -377,7 +377,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=None, help="override N (rows per GPU)")
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=None,
+                    help="override N (rows per GPU); use --rows under torchrun, whose parser claims --n")
     ap.add_argument("--ref-sample", type=int, default=1 << 13, help="rows per reference step (bounded sample)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 13)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -408,10 +409,18 @@ def main():
     from paper_2205_02990_b200 import synthetic
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HBS_BENCH_BACKEND=gloo: functional check of the N > 1 path on a box with fewer GPUs than ranks
+    # (ranks share devices, host-staged gather; its timings mean nothing)
+    backend = os.environ.get("HBS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     N, k, leaf, s, r, decay = cfg
     if world > 1:
         run_distributed(args, cfg, world, rank, dev)
