@@ -429,16 +429,17 @@ def _charge_madds(tree: ClusterTree, s: int, r: int):
     flops.add_madds(total)
 
 
-def _pinned_view(a):
-    """torch view of a numpy array if it lives in pinned host memory, else None."""
+def _host_view(a):
+    """torch view of a host numpy array (float64, C-contiguous; copied only if
+    it is not), else None for device tensors."""
     if isinstance(a, torch.Tensor):
         return None
-    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-    return t if t.is_pinned() else None
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
 
 
 def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, dev, chunks: int = None):
-    """Host (pinned) samples in, host-materialised factorization out, with the
+    """Host samples in (pinned, or pageable staged through pinned buffers),
+    host-materialised factorization out, with the
     transfers hidden behind the compute by subtree: the rows are uploaded as
     `chunks` contiguous subtrees (one H2D stream), each subtree is compressed
     from its leaves up to its own root as soon as its rows have arrived (the
@@ -505,19 +506,40 @@ def _compress_host_subtrees(host, tree: ClusterTree, config: CompressionConfig, 
     # behind gigabytes of H2D on the copy engine)
     if _t is not None:
         _t.append(time.perf_counter())
-    arrived = []
-    for p in parts:              # all uploads back to back on the H2D stream
+    def upload(p, src):          # rows of one subtree, host -> device on the H2D stream
         with torch.cuda.stream(h2d):
             for i in range(4):
-                dq[i][p.begin:p.end].copy_(host[i][p.begin:p.end], non_blocking=True)
+                dq[i][p.begin:p.end].copy_(src[i], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(h2d)
-        arrived.append(ev)
+        return ev
 
-    for p, ev, plan in zip(parts, arrived, plans):
-        comp.wait_event(ev)
-        plan.run(*[m[p.begin:p.end] for m in dq], stream=comp.cuda_stream)
-        drain(p.local_specs, plan)
+    if all(h.is_pinned() for h in host):
+        # all uploads back to back on the H2D stream, then the launches
+        arrived = [upload(p, [h[p.begin:p.end] for h in host]) for p in parts]
+        for p, ev, plan in zip(parts, arrived, plans):
+            comp.wait_event(ev)
+            plan.run(*[m[p.begin:p.end] for m in dq], stream=comp.cuda_stream)
+            drain(p.local_specs, plan)
+    else:
+        # ordinary (pageable) numpy arrays, the reference's calling convention:
+        # each subtree's rows are staged through one of two pinned buffer sets
+        # (a multi-threaded host copy) while the previous subtree is in flight
+        rows = max(p.end - p.begin for p in parts)
+        stage = [[torch.empty(rows, s, dtype=f64, pin_memory=True) for _ in range(4)] for _ in range(2)]
+        in_flight = [None, None]
+        for idx, (p, plan) in enumerate(zip(parts, plans)):
+            buf = stage[idx % 2]
+            if in_flight[idx % 2] is not None:
+                in_flight[idx % 2].synchronize()      # the upload that last used this buffer set
+            nr = p.end - p.begin
+            for i in range(4):
+                buf[i][:nr].copy_(host[i][p.begin:p.end])
+            ev = upload(p, [b[:nr] for b in buf])
+            in_flight[idx % 2] = ev
+            comp.wait_event(ev)
+            plan.run(*[m[p.begin:p.end] for m in dq], stream=comp.cuda_stream)
+            drain(p.local_specs, plan)
     if world > 1:
         with torch.cuda.stream(comp):
             top_quad = tuple(torch.cat([pl.top_quad[i] for pl in plans]) for i in range(4))
@@ -564,9 +586,9 @@ def compress_from_samples(samples: SampleSet, tree: ClusterTree, config: Compres
         dev = torch.device(device)
     if dev.type != "cuda":
         raise DimensionError("the compressor runs on a CUDA device only (no CPU fallback)")
-    pinned = [_pinned_view(m) for m in (samples.omega, samples.psi, samples.y, samples.z)]
-    if all(p is not None for p in pinned) and tree.depth >= 2:
-        f = _compress_host_subtrees(pinned, tree, config, dev)
+    hostv = [_host_view(m) for m in (samples.omega, samples.psi, samples.y, samples.z)]
+    if all(h is not None for h in hostv) and tree.depth >= 2:
+        f = _compress_host_subtrees(hostv, tree, config, dev)
         if flops.counting():
             _charge_madds(tree, s, r)
         return f

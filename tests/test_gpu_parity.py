@@ -270,20 +270,23 @@ def _pinned(a):
 
 @pytest.mark.parametrize("name", ["c1_twin", "uneven_333", "c4_shape_literal"])
 def test_pinned_host_pipeline_bitwise(name):
-    """Pinned host samples take the overlapped path (subtree-chunked uploads,
-    per-level downloads on a second stream); results equal the plain path
-    bit for bit, and the dict views come back already on the host."""
+    """Host samples take the overlapped path (subtree-chunked uploads -- pinned
+    arrays directly, pageable numpy arrays staged through pinned buffers --,
+    per-level downloads on a second stream); results equal the plain level
+    sweep on device-resident samples bit for bit, and the dict views come back
+    already on the host."""
     c = golden_cases.load(name)
     tree = hb.build_tree(c["n"], c["leaf"])
     cfg = hb.CompressionConfig(rank=c["r"], leaf_threshold=c["leaf"])
-    plain = hb.compress_from_samples(hb.SampleSet(*c["samples"]), tree, cfg)
+    plain = hb.compress_from_samples(hb.SampleSet(*(torch.from_numpy(m).cuda() for m in c["samples"])), tree, cfg)
     keep = [_pinned(m) for m in c["samples"]]
-    piped = hb.compress_from_samples(hb.SampleSet(*(t.numpy() for t in keep)), tree, cfg)
-    assert ("root" in piped._host) and all((lv, "d") in piped._host for lv in range(1, tree.depth + 1))
-    assert np.array_equal(plain.root_disc, piped.root_disc)
-    for nid in plain.u_bases:
-        assert np.array_equal(plain.u_bases[nid], piped.u_bases[nid])
-        assert np.array_equal(plain.discs[nid], piped.discs[nid])
+    for piped in (hb.compress_from_samples(hb.SampleSet(*(t.numpy() for t in keep)), tree, cfg),
+                  hb.compress_from_samples(hb.SampleSet(*c["samples"]), tree, cfg)):
+        assert ("root" in piped._host) and all((lv, "d") in piped._host for lv in range(1, tree.depth + 1))
+        assert np.array_equal(plain.root_disc, piped.root_disc)
+        for nid in plain.u_bases:
+            assert np.array_equal(plain.u_bases[nid], piped.u_bases[nid])
+            assert np.array_equal(plain.discs[nid], piped.discs[nid])
 
 
 def test_pinned_host_pipeline_failure_names_node():
