@@ -446,3 +446,32 @@ def test_sigma_screen_window_is_one_sided():
         hb.lstsq_right(b, m, 2.0 * diag_ratio)
     x, _ = O.right_solve(b, m, 2.0 * diag_ratio)
     assert x is None
+
+
+def test_level_hint_does_not_change_results():
+    """hbs_level_hint only lets the library skip launches that would find no
+    box: a sweep whose levels are hinted as uniform (the default) and one with
+    the hint withheld (min_rows = 0: unknown) leave the same bits, and the
+    hinted sweep performs fewer launches."""
+    import torch
+    from paper_2205_02990_b200 import synthetic
+    n, leaf, k, s = 1 << 12, 128, 64, 192
+    tree = hb.build_tree(n, leaf)
+    gen = synthetic.device_generator(tree, k, seed=4, decay=0.9)
+    quad = synthetic.device_samples(gen, s)
+    lib = hb._native.lib()
+    outs, launches = [], []
+    for hinted in (True, False):
+        plan = hb.CompressPlan(tree, s, k)
+        if not hinted:
+            for g in plan.geometry.values():
+                g.min_rows = 0
+        n0 = lib.hbs_launch_counter()
+        plan.run(*quad)
+        torch.cuda.synchronize()
+        plan.raise_for_status()
+        launches.append(lib.hbs_launch_counter() - n0)
+        outs.append([m.clone() for lv in sorted(plan.levels) for m in plan.levels[lv]] + [plan.root.clone()])
+    assert launches[0] < launches[1]
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
