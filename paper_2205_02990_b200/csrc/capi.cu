@@ -39,6 +39,28 @@ struct PhaseTimer {
 };
 PhaseTimer g_timer;  // only used by the profiled entry point (not thread-safe by design)
 
+// Side stream for the four lift products that need only the bases (V^T Omega,
+// U^T Psi, U^T Y, V^T Z): they run next to the discrepancy chain, which matters
+// on the upper levels where a single short GEMM cannot fill the GPU.  Forked
+// and joined with events, so a CUDA-graph capture of the caller's stream keeps
+// the concurrency.  HBS_LIFT_OVERLAP=0 keeps everything on one stream.
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+  SideStream() {
+    const char* e = std::getenv("HBS_LIFT_OVERLAP");
+    if (e && e[0] == '0') return;
+    ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+SideStream& side_stream() {
+  thread_local SideStream s;
+  return s;
+}
+
 constexpr size_t kAlign = 256;
 
 // HBS_GRAM_V3=1: the one-CTA-per-SM Gram kernel (gram.cu) instead of the TMEM one (gram_tm.cu)
@@ -320,6 +342,29 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   const BOperand Vt = op(v, r, 0, 0, r, false, true);
   const BOperand Vn = op(v, r, 0, 0, r, false, false);
   const int64_t sqs = (int64_t)nr * nr, rs = (int64_t)r * nr;
+  const BOperand Om = op(omega, s, 0, 0, s, false, false);
+  const BOperand Ps = op(psi, s, 0, 0, s, false, false);
+  const BOperand Yn = op(y, s, 0, 0, s, false, false);
+  const BOperand Zn = op(z, s, 0, 0, s, false, false);
+  const int64_t prs = (int64_t)r * s;
+  // the lift products that need only the bases go to the side stream (not under the
+  // phase timer, whose events live on the caller's stream)
+  SideStream& side = side_stream();
+  const bool overlap = lift_omega != nullptr && side.ok && !g_timer.on;
+  cudaStream_t ls = overlap ? side.st : st;
+  auto lift_base = [&]() -> int {
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Om, lift_omega, 0, prs, 0, s, false, 1.0, 0.0, none, ls));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Ps, lift_psi, 0, prs, 0, s, false, 1.0, 0.0, none, ls));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Yn, lift_y, 0, prs, 0, s, false, 1.0, 0.0, none, ls));
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Zn, lift_z, 0, prs, 0, s, false, 1.0, 0.0, none, ls));
+    return HBS_OK;
+  };
+  if (overlap) {
+    if (cudaEventRecord(side.fork, st) != cudaSuccess || cudaStreamWaitEvent(side.st, side.fork, 0) != cudaSuccess)
+      return HBS_ERR_CUDA;
+    HBS_TRY(lift_base());
+    if (cudaEventRecord(side.join, side.st) != cudaSuccess) return HBS_ERR_CUDA;
+  }
   const BOperand Xn = op(w.Xp[0], 0, w.strideX, 0, w.ldX, false, false);
   const BOperand Wt = op(w.Xp[1], 0, w.strideX, 0, w.ldX, false, true);
   const BOperand G1 = op(w.G1, 0, rs, 0, nr, false, false);
@@ -341,17 +386,13 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     // U^T D = E1 from the discrepancy algebra (U^T U = I); V^T D^T directly
     const BOperand E2 = op(w.E2, 0, rs, 0, nr, false, false);
     HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Vt, Dt, w.E2, 0, rs, 0, nr, false, 1.0, 0.0, none, st));
-    const BOperand Om = op(omega, s, 0, 0, s, false, false);
-    const BOperand Ps = op(psi, s, 0, 0, s, false, false);
-    const BOperand Yn = op(y, s, 0, 0, s, false, false);
-    const BOperand Zn = op(z, s, 0, 0, s, false, false);
-    const int64_t prs = (int64_t)r * s;
-    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Om, lift_omega, 0, prs, 0, s, false, 1.0, 0.0, none, st));
-    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Ps, lift_psi, 0, prs, 0, s, false, 1.0, 0.0, none, st));
-    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Ut, Yn, lift_y, 0, prs, 0, s, false, 1.0, 0.0, none, st));
+    if (overlap) {
+      if (cudaStreamWaitEvent(st, side.join, 0) != cudaSuccess) return HBS_ERR_CUDA;
+    } else {
+      HBS_TRY(lift_base());
+    }
     HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E1, Om, lift_y, 0, prs, 0, s, false, -1.0, 1.0,
                  op(lift_y, 0, prs, 0, s, false, false), st));
-    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, Vt, Zn, lift_z, 0, prs, 0, s, false, 1.0, 0.0, none, st));
     HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E2, Ps, lift_z, 0, prs, 0, s, false, -1.0, 1.0,
                  op(lift_z, 0, prs, 0, s, false, false), st));
   }
