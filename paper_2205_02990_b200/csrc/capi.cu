@@ -46,13 +46,14 @@ PhaseTimer g_timer;  // only used by the profiled entry point (not thread-safe b
 // the concurrency.  HBS_LIFT_OVERLAP=0 keeps everything on one stream.
 struct SideStream {
   cudaStream_t st = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, e1 = nullptr, join = nullptr;
   bool ok = false;
   SideStream() {
     const char* e = std::getenv("HBS_LIFT_OVERLAP");
     if (e && e[0] == '0') return;
     ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
          cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
@@ -363,7 +364,6 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
     if (cudaEventRecord(side.fork, st) != cudaSuccess || cudaStreamWaitEvent(side.st, side.fork, 0) != cudaSuccess)
       return HBS_ERR_CUDA;
     HBS_TRY(lift_base());
-    if (cudaEventRecord(side.join, side.st) != cudaSuccess) return HBS_ERR_CUDA;
   }
   const BOperand Xn = op(w.Xp[0], 0, w.strideX, 0, w.ldX, false, false);
   const BOperand Wt = op(w.Xp[1], 0, w.strideX, 0, w.ldX, false, true);
@@ -376,6 +376,13 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
   // E1 = G1 - M3 V^T (= U^T D, reused by the lift), M4 = U^T X - E1
   const BOperand E1 = op(w.E1, 0, rs, 0, nr, false, false);
   HBS_TRY(gemm(geo, dfix(r), drows(), dfix(r), r, nr, M3, Vt, w.E1, 0, rs, 0, nr, false, -1.0, 1.0, G1, st));
+  if (overlap) {   // U^T (Y - D Omega) = U^T Y - E1 Omega needs nothing beyond E1: finish it on the side stream
+    if (cudaEventRecord(side.e1, st) != cudaSuccess || cudaStreamWaitEvent(side.st, side.e1, 0) != cudaSuccess)
+      return HBS_ERR_CUDA;
+    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E1, Om, lift_y, 0, prs, 0, s, false, -1.0, 1.0,
+                 op(lift_y, 0, prs, 0, s, false, false), side.st));
+    if (cudaEventRecord(side.join, side.st) != cudaSuccess) return HBS_ERR_CUDA;
+  }
   HBS_TRY(gemm(geo, dfix(r), drows(), drows(), r, nr, Ut, Xn, w.M4, 0, rs, 0, nr, false, 1.0, -1.0, E1, st));
   HBS_TRY(gemm(geo, drows(), drows(), dfix(r), nr, nr, Un, M4, d, 0, 0, 1, 0, true, -1.0, 1.0, Xn, st));
   g_timer.mark();
@@ -390,9 +397,9 @@ int hbs_compress_level(int64_t nbox, const int64_t* row_begin, const int64_t* sq
       if (cudaStreamWaitEvent(st, side.join, 0) != cudaSuccess) return HBS_ERR_CUDA;
     } else {
       HBS_TRY(lift_base());
+      HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E1, Om, lift_y, 0, prs, 0, s, false, -1.0, 1.0,
+                   op(lift_y, 0, prs, 0, s, false, false), st));
     }
-    HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E1, Om, lift_y, 0, prs, 0, s, false, -1.0, 1.0,
-                 op(lift_y, 0, prs, 0, s, false, false), st));
     HBS_TRY(gemm(geo, dfix(r), dfix(s), drows(), r, s, E2, Ps, lift_z, 0, prs, 0, s, false, -1.0, 1.0,
                  op(lift_z, 0, prs, 0, s, false, false), st));
   }
