@@ -357,7 +357,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   double* T = Tscr + 384;
   double* A = T + round_up(kP * kLdT, 2);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_ready + 34);
-  int* s_pflag = reinterpret_cast<int*>(s_ready + 34) + 1;   // panel_factor_gram verdict
 
   // load Omega^T (s x n col-major == Omega rows), zero rows m .. mpad-1.
   // Each column is one contiguous Omega row: TMA bulk copies (one per column)
@@ -370,11 +369,7 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   // TMEM columns of this CTA: the Y rows (2 b32 columns per fp64 column) up to the
   // solve's padded width; small boxes leave room for the other CTAs of the SM
-#ifdef HBS_PRE_PAIRS
-  const uint32_t tcols = 512;
-#else
   const uint32_t tcols = TM ? tm_pow2_cols(2 * min(256, max(round_up(s, 16), round_up(n, 32) + 16))) : 0;
-#endif
   if (TM && warp == 0) tm_alloc(s_tmem, tcols);
   tm_fence_before();
   __syncthreads();
@@ -457,237 +452,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
       __syncwarp();
     }
   };
-#ifdef HBS_PRE_PAIRS   // experiment: measured slower (the T prologue is exposed), PRE at 8 Y warps is the default
-  if constexpr (PRE && TM) {
-    if (s <= 192) {
-      // ---------------------------------------------------------- PRE, paired
-      // The factorisation is final, so all 16 warps apply it: warp pair
-      // (pi, pi + 8) owns TMEM rows R0 .. R0+15; warp half h computes the
-      // products of its row group (rows R0 + 8h + g) and updates half of the
-      // column chunks of Y for both row groups.  The two halves exchange
-      // W2 = (Y V_p) T_p through the TMEM columns beyond Y (2s + 128 <= 512).
-      const uint32_t tbase = *s_tmem;
-      const int pi = warp & 7, half = warp >> 3;
-      const int R0 = 32 * (pi & 3) + 16 * (pi >> 2);
-      const uint32_t tl = tbase + ((uint32_t)R0 << 16);
-      const int rowh[2] = {R0 + g, R0 + 8 + g};
-      const bool okh[2] = {R0 + g < nb, R0 + 8 + g < nb};
-      const int sig = (g >> 1) + ((g & 1) ? 4 : 0);
-      const int spad = round_up(s, 8), scol = round_up(s, 16);
-      const int xcol[2] = {192, 224};                 // fp64 exchange columns of the two halves
-      const int pbar = 3 + pi;
-      auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(pbar) : "memory"); };
-      if (half) {
-        // panel T (dlarft from V^T V and the Gram kernel's tau) and R's
-        // diagonal-block inverses, by the upper half (group barrier 1)
-        const int lt = threadIdx.x ^ 256;
-        for (int p = 0; p < npanel; ++p) {
-          const int j0 = p * kP, nbp = min(kP, n - j0);
-          for (int e = lt; e < nbp; e += 256) s_tau[j0 + e] = tglob[(size_t)p * kP * kP + e];
-          gsync<256>();
-          panel_gram<256>(A, lda, m, j0, nbp, G);
-          gsync<256>();
-          form_t<256>(T, Tscr, G, s_tau, j0, nbp);
-          for (int e = lt; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
-          gsync<256>();
-          tri_inverse32<256, 1>(A, lda, j0, nbp, rglob + (size_t)p * kP * kP, Tscr, 8);
-          gsync<256>();
-        }
-      } else {
-        // Y rows into TMEM (columns s .. zero: the solve's padded blocks)
-        const int zcol = min(2 * 96, max(scol, round_up(n, 32) + 16));
-        const double* y0 = S.y + S.y_c_rb * rb;
-        for (int c0 = 0; c0 < zcol; c0 += 16) {
-          double v[4][2];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = c0 + 4 * q + t;
-              v[q][h] = (okh[h] && c < s) ? __ldcs(y0 + (size_t)rowh[h] * s + c) : 0.0;
-            }
-          tm_st16(tl + 2 * c0, v);
-        }
-        tm_wait_st();
-      }
-      __threadfence_block();
-      tm_fence_before();
-      __syncthreads();
-      tm_fence_after();
-      for (int p = 0; p < npanel; ++p) {
-        const int j0 = p * kP, nbp = min(kP, n - j0), kb = j0 & ~7;
-        const double* tp = tglob + (size_t)p * kP * kP;
-        // GEMM1: W = Y(my rows, kb:) V_p   (8 x 32)
-        double w[4][2] = {};
-        for (int kc = kb & ~15; kc < spad; kc += 16) {
-          double a[4][2];
-          tm_ld16(tl + 2 * kc, a);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int k = kc + 4 * u;
-            if (k < kb) continue;
-            if (k >= spad) break;
-            const double av = half ? a[u][1] : a[u][0];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const double bv = (k < j0 + kP) ? vval(A, lda, j0, nbp, k + t, 8 * f + g)
-                                              : ((8 * f + g < nbp) ? A[(k + t) + (j0 + 8 * f + g) * lda] : 0.0);
-              dmma8x8x4(w[f][0], w[f][1], av, bv);
-            }
-          }
-        }
-        // GEMM2: W2 = W T_p
-        double w2[4][2] = {};
-#pragma unroll
-        for (int kk = 0; kk < kP; kk += 4) {
-          const double a0 = cfrag_to_afrag<4>(w, kk, lane);
-#pragma unroll
-          for (int f = 0; f < 4; ++f) dmma8x8x4(w2[f][0], w2[f][1], a0, __ldcg(tp + (kk + t) * kP + 8 * f + g));
-        }
-        double a3[2][kP / 4];
-#pragma unroll
-        for (int kk = 0; kk < kP; kk += 4) a3[half][kk / 4] = -cfrag_to_afrag<4>(w2, kk, lane);
-        // exchange -W2 (A fragments) with the partner through TMEM
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          double v[4][2];
-#pragma unroll
-          for (int rep = 0; rep < 4; ++rep) { v[rep][0] = a3[half][4 * q + rep]; v[rep][1] = a3[half][4 * q + rep]; }
-          tm_st16(tl + 2 * (xcol[half] + 16 * q), v);
-        }
-        tm_wait_st();
-        tm_fence_before();
-        pair_sync();
-        tm_fence_after();
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          double v[4][2];
-          tm_ld16(tl + 2 * (xcol[1 - half] + 16 * q), v);
-#pragma unroll
-          for (int rep = 0; rep < 4; ++rep) a3[1 - half][4 * q + rep] = half ? v[rep][0] : v[rep][1];
-        }
-        // GEMM3: Y(:, kb:) -= W2 V_p^T on my half of the 16-column chunks
-        int ci = 0;
-        for (int nc = kb & ~15; nc < spad; nc += 16, ++ci) {
-          if ((ci & 1) != half) continue;
-          double cv[4][2];
-          tm_ld16(tl + 2 * nc, cv);
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb) {
-            const int n0 = nc + 8 * hb;
-            if (n0 < kb || n0 >= spad) continue;
-            const int col = n0 + sig;
-#pragma unroll
-            for (int kk = 0; kk < kP; kk += 4) {
-              const double bv = (n0 < j0 + kP) ? vval(A, lda, j0, nbp, col, kk + t)
-                                               : ((kk + t < nbp) ? A[col + (j0 + kk + t) * lda] : 0.0);
-              dmma8x8x4(cv[2 * hb][0], cv[2 * hb + 1][0], a3[0][kk / 4], bv);
-              dmma8x8x4(cv[2 * hb][1], cv[2 * hb + 1][1], a3[1][kk / 4], bv);
-            }
-          }
-          tm_st16(tl + 2 * nc, cv);
-        }
-        tm_wait_st();
-        tm_fence_before();
-        pair_sync();
-        tm_fence_after();
-      }
-      // blocked back substitution X R^T = Y Q1 on the TMEM rows (lower half of each pair)
-      if (!half) {
-        for (int blk = npanel - 1; blk >= 0; --blk) {
-          const int i0 = blk * kP, c0 = i0 + kP;
-          const int kr = n > c0 ? round_up(n - c0, 4) : 0;
-          double acc[2][4][2];
-          {
-            double v[4][2];
-#pragma unroll
-            for (int hq = 0; hq < 2; ++hq) {
-              tm_ld16(tl + 2 * (i0 + 16 * hq), v);
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                acc[h][2 * hq][0] = v[0][h]; acc[h][2 * hq][1] = v[1][h];
-                acc[h][2 * hq + 1][0] = v[2][h]; acc[h][2 * hq + 1][1] = v[3][h];
-              }
-            }
-          }
-          for (int kc = 0; kc < kr; kc += 16) {
-            double av[4][2];
-            tm_ld16(tl + 2 * (c0 + kc), av);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int k = kc + 4 * u;
-              if (k >= kr) break;
-              const int c = c0 + k + t;
-#pragma unroll
-              for (int f = 0; f < 4; ++f) {
-                const int i = i0 + 8 * f + sig;
-                const double bv = (i < n && c < n) ? A[i + c * lda] : 0.0;   // R(i, c)
-                dmma8x8x4(acc[0][f][0], acc[0][f][1], -av[u][0], bv);
-                dmma8x8x4(acc[1][f][0], acc[1][f][1], -av[u][1], bv);
-              }
-            }
-          }
-          const double* ri = rglob + (size_t)blk * kP * kP;
-          double xb[2][4][2] = {};
-#pragma unroll
-          for (int kk = 0; kk < kP; kk += 4) {
-            const double a0 = cfrag_to_afrag<4>(acc[0], kk, lane);
-            const double a1 = cfrag_to_afrag<4>(acc[1], kk, lane);
-            const int kq = (kk & 7) + t;
-            const int kact = 8 * (kk >> 3) + (kq >> 1) + ((kq & 1) ? 4 : 0);
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const double bv = __ldcg(ri + (8 * f + sig) * kP + kact);
-              dmma8x8x4(xb[0][f][0], xb[0][f][1], a0, bv);
-              dmma8x8x4(xb[1][f][0], xb[1][f][1], a1, bv);
-            }
-          }
-          {
-            double v[4][2];
-#pragma unroll
-            for (int hq = 0; hq < 2; ++hq) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int ff = 0; ff < 2; ++ff) {
-                  const int f = 2 * hq + ff;
-                  const int cA = i0 + 8 * f + t, cB = cA + 4;
-                  v[2 * ff][h] = cA < n ? xb[h][f][0] : acc[h][f][0];
-                  v[2 * ff + 1][h] = cB < n ? xb[h][f][1] : acc[h][f][1];
-                }
-              tm_st16(tl + 2 * (i0 + 16 * hq), v);
-            }
-          }
-          tm_wait_st();
-        }
-      }
-      tm_fence_before();
-      pair_sync();
-      tm_fence_after();
-      // Y Q (X in columns < n, Y P in columns s-r .. s-1) to the workspace, half the chunks each
-      {
-        int ci = 0;
-        for (int c0 = 0; c0 < scol; c0 += 16, ++ci) {
-          if ((ci & 1) != half) continue;
-          double v[4][2];
-          tm_ld16(tl + 2 * c0, v);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = c0 + 4 * q + t;
-              if (okh[h] && c < s) yq[(size_t)rowh[h] * s + c] = v[q][h];
-            }
-        }
-      }
-      tm_fence_before();
-      __syncthreads();
-      tm_fence_after();
-      if (warp == 0) tm_dealloc(tbase, tcols);
-      return;
-    }
-  }
-#endif
   // s_ready[p] (p < 16): panel p factored (P -> Y);  s_ready[16 + p]: far
   // trailing update of panel p done (Y -> P);  s_ready[32]: all panels
   // applied to YQ (Y -> P);  s_ready[33]: operand load (TMA).
@@ -723,20 +487,12 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
         gsync<256>();
       }
       if (lt == 0) FUSED_MARK(22 + 2 * p);
-#ifdef HBS_GRAM_PANEL   // experiment (measured slower: the single-warp 32-step factorisations)
-      const bool gp = panel_factor_gram<256>(A, lda, m, j0, nbp, G, T, Tscr, s_pflag);
-#else
-      const bool gp = false;
-      (void)s_pflag;
-#endif
-      if (!gp) {
-        // Householder chain; the step barriers complete once per chain-factored panel
-        if constexpr (MR <= 6) panel_factor_r<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
-        else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
-        ++nhh;
-      }
+      // Householder chain; the step barriers complete once per panel
+      if constexpr (MR <= 6) panel_factor_r<MR, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
+      else panel_factor_wide<MR, 8, 256>(A, lda, m, j0, nbp, s_tau, s_scale, s_beta, s_bar, (unsigned)(nhh & 1), G);
+      ++nhh;
       if (lt == 0) FUSED_MARK(42 + p);
-      if (!gp) form_t<256>(T, Tscr, G, s_tau, j0, nbp);
+      form_t<256>(T, Tscr, G, s_tau, j0, nbp);
       for (int e = lt; e < kP * kP; e += 256) tglob[(size_t)p * kP * kP + e] = T[(e / kP) * kLdT + e % kP];
       __threadfence_block();
       gsync<256>();
@@ -967,16 +723,6 @@ __global__ void __launch_bounds__(512, 1) probe_fused_kernel(FusedArgs args) {
     if (yw == 0 && lane == 0) FUSED_MARK(41);
     return;
   }
-#ifdef HBS_TRACE_NOY
-  // timing experiment only: keep the far-trailing / ready hand-shakes, skip the Y work
-  for (int p = 0; p < npanel; ++p) {
-    mbar_wait(&s_ready[p], 0);
-    if (p * kP + 2 * kP < n) { ysync<256, 2>(); if (yw == 0 && lane == 0) mbar_arrive(&s_ready[16 + p]); }
-  }
-  ysync<256, 2>();
-  if (yw == 0 && lane == 0) mbar_arrive(&s_ready[32]);
-  return;
-#endif
   const double* y0 = S.y + S.y_c_rb * rb;
   // 16-byte vector accesses only when every row start is 16-byte aligned
   const bool vec2 = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(y0) & 15) == 0) &&

@@ -231,218 +231,6 @@ HBS_DEV void block_reflector_apply(double* A, int lda, int mpad, int j0, int nbp
   }
 }
 
-// Factor panel j0 (nbp <= 32 columns) in place.  Leaves: pre-scale reflector
-// values in A (finalised afterwards by the caller), tau/scale/beta in smem,
-// G(c, j) = v_c . v_j (c < j) in G.
-// Panel factorisation in 8-column sub-panels.  In sub-panel q, warp w < 8 owns
-// column cs + w (cs = j0 + 8q) in registers (rows j0 + lane + 32k).  Step j
-// needs only pivot j: its owner publishes (column in A, tau/scale/beta in
-// smem) and arrives on bar[j]; the others wait on bar[j] alone.  bar[] completes
-// once per panel (parity = panel & 1).  The owners of earlier sub-panel columns
-// form the compact-WY dots v_c . v_j on the fly (G8); after the 8 steps the
-// sub-panel's block reflector is applied to the rest of the panel on the
-// tensor cores, so only 8 warps ever contend for issue during a step.
-template <int MR, int NTG>
-HBS_DEV void panel_factor(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
-                          double* s_beta, uint64_t* bar, unsigned parity, double* G8, double* T8,
-                          double* wpart, double* wfin) {
-  constexpr int kSub = 8;
-  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int kc = (m - j0 + 31) >> 5;  // row blocks of 32 from j0 (storage padded to 32)
-  for (int cs = j0; cs < j0 + nbp; cs += kSub) {
-    const int nsub = min(kSub, j0 + nbp - cs);
-    const int jq = cs - j0;           // step index of the sub-panel's first pivot
-    if (warp < nsub) {
-      const int c = cs + warp;
-      double x[MR];
-#pragma unroll
-      for (int k = 0; k < MR; ++k) x[k] = (k < kc) ? A[(j0 + lane + 32 * k) + c * lda] : 0.0;
-      if (warp == 0) {  // first pivot of the sub-panel: exact norm
-        double p = 0.0;
-#pragma unroll
-        for (int k = 0; k < MR; ++k) {
-          const int row = j0 + lane + 32 * k;
-          if (k < kc && row > cs) p = fma(x[k], x[k], p);
-        }
-        p = warp_sum(p);
-        const double alpha = __shfl_sync(0xffffffffu, x[0], jq);   // row cs: slot 0, lane jq (< 32)
-        if (lane == 0) {
-          const Reflector h = make_reflector(alpha, p);
-          s_tau[cs] = h.tau; s_scale[cs] = h.scale; s_beta[cs] = h.beta;
-          mbar_arrive(&bar[jq]);
-          HQR_STEP(jq);
-        }
-      }
-      for (int i = 0; i < nsub; ++i) {
-        const int jj = cs + i, j = jq + i;
-        if (c == jj) continue;
-        mbar_wait(&bar[j], parity);
-        const double tau = s_tau[jj], scale = s_scale[jj];
-        double pv[MR];
-#pragma unroll
-        for (int k = 0; k < MR; ++k) {
-          const int row = j0 + lane + 32 * k;
-          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
-        }
-        const bool pub = (c == jj + 1);   // I publish the next pivot
-        double d = 0.0, sxx = 0.0, spp = 0.0;
-#pragma unroll
-        for (int k = 0; k < MR; ++k) {
-          d = fma(pv[k], x[k], d);
-          if (pub) {
-            const int row = j0 + lane + 32 * k;
-            if (row > jj + 1) { sxx = fma(x[k], x[k], sxx); spp = fma(pv[k], pv[k], spp); }
-          }
-        }
-        const double rj = __shfl_sync(0xffffffffu, x[0], j);   // my value in row jj (slot 0, lane j < 32)
-        double xn_old = 0.0, pn = 0.0;
-        if (pub) {
-          pn = __shfl_sync(0xffffffffu, pv[0], j + 1);
-          xn_old = __shfl_sync(0xffffffffu, x[0], j + 1);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          d += __shfl_xor_sync(0xffffffffu, d, o);
-          if (pub) {
-            sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
-            spp += __shfl_xor_sync(0xffffffffu, spp, o);
-          }
-        }
-        if (c < jj) {   // compact-WY dot v_c . v_jj (my column is a retired reflector)
-          if (lane == 0) G8[(c - cs) * kSub + i] = s_scale[c] * (rj + scale * d);
-          continue;
-        }
-        const double f = tau * (rj + scale * d), gs = f * scale;
-#pragma unroll
-        for (int k = 0; k < MR; ++k) x[k] = fma(-gs, pv[k], x[k]);
-        if (lane == j) x[0] -= f;
-        if (pub) {
-          const double sxp = d - pn * xn_old;
-          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, sxp, sxx));
-          if (!(nrm > 0.5 * sxx) || sxx == 0.0) {   // cancellation: recompute exactly
-            double p = 0.0;
-#pragma unroll
-            for (int k = 0; k < MR; ++k) {
-              const int row = j0 + lane + 32 * k;
-              if (k < kc && row > jj + 1) p = fma(x[k], x[k], p);
-            }
-            nrm = warp_sum(p);
-          }
-#pragma unroll
-          for (int k = 0; k < MR; ++k)
-            if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
-          const double alpha = __shfl_sync(0xffffffffu, x[0], j + 1);
-          __syncwarp();
-          if (lane == 0) {
-            const Reflector h = make_reflector(alpha, nrm);
-            s_tau[c] = h.tau; s_scale[c] = h.scale; s_beta[c] = h.beta;
-            mbar_arrive(&bar[j + 1]);
-            HQR_STEP(j + 1);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < MR; ++k)
-        if (k < kc) A[(j0 + lane + 32 * k) + c * lda] = x[k];
-    }
-    gsync<NTG>();
-    if (ltid<NTG>() == 0) HQR_STEP(40 + (jq >> 3) * 4);
-    // finalise the sub-panel: v tails = x * scale, diagonal = beta
-    for (int q = 0; q < nsub; ++q) {
-      const int c = cs + q;
-      const double sc = s_scale[c];
-      for (int i = c + ltid<NTG>(); i < m; i += gthreads<NTG>()) {
-        if (i > c) A[i + c * lda] *= sc;
-        else A[i + c * lda] = s_beta[c];
-      }
-    }
-    const int c1 = cs + kSub, c2 = j0 + nbp;   // remaining panel columns
-    if (c1 < c2) {
-      // T8 (dlarft recurrence, lanes 0..7 of warp 0); meanwhile warps 1..4
-      // form partial W = V_sub^T X_rest over K chunks.
-      if (warp == 0) {
-        if (lane < kSub) {
-          double trow[kSub];
-#pragma unroll
-          for (int cc = 0; cc < kSub; ++cc) {
-            const double tc = (cc < nsub) ? s_tau[cs + cc] : 0.0;
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < cc; ++q)
-              if (q >= lane) acc = fma(trow[q], G8[q * kSub + cc], acc);
-            trow[cc] = (lane < cc) ? -tc * acc : (lane == cc ? tc : 0.0);
-          }
-#pragma unroll
-          for (int cc = 0; cc < kSub; ++cc) T8[lane * kSub + cc] = trow[cc];
-        }
-      }
-      gsync<NTG>();   // finalised V visible
-      if (ltid<NTG>() == 0) HQR_STEP(41 + (jq >> 3) * 4);
-      const int kspan = round_up(m - cs, 4);
-      const int nsplit = 4;
-      const int kchunk = round_up((kspan + nsplit - 1) / nsplit, 4);
-      if (warp >= 1 && warp <= nsplit) {
-        const int ws = warp - 1;
-        const int kb = cs + ws * kchunk, ke = min(cs + kspan, kb + kchunk);
-        double w[3][2] = {};
-        for (int k = kb; k < ke; k += 4) {
-          const int i = k + t;
-          // A = V_sub^T (row g = reflector, col = row index i)
-          const double av = (g < nsub && i >= cs + g) ? (i == cs + g ? 1.0 : A[i + (cs + g) * lda]) : 0.0;
-#pragma unroll
-          for (int f = 0; f < 3; ++f) {
-            const int cc = c1 + 8 * f + g;
-            const double bv = cc < c2 ? A[i + cc * lda] : 0.0;
-            dmma8x8x4(w[f][0], w[f][1], av, bv);
-          }
-        }
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          wpart[ws * 192 + g * 24 + 8 * f + 2 * t] = w[f][0];
-          wpart[ws * 192 + g * 24 + 8 * f + 2 * t + 1] = w[f][1];
-        }
-      }
-      gsync<NTG>();
-      if (ltid<NTG>() == 0) HQR_STEP(42 + (jq >> 3) * 4);
-      // W' = T8^T (sum of partials)  (8 x 24)
-      for (int e = ltid<NTG>(); e < 192; e += gthreads<NTG>()) {
-        const int q = e / 24, cc = e % 24;
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < kSub; ++a) {
-          const double wa = wpart[a * 24 + cc] + wpart[192 + a * 24 + cc] + wpart[384 + a * 24 + cc] +
-                            wpart[576 + a * 24 + cc];
-          acc = fma(T8[a * kSub + q], wa, acc);
-        }
-        wfin[e] = acc;
-      }
-      gsync<NTG>();
-      // X_rest(rows cs.., c1..c2) -= V_sub W'
-      const int nrb = (round_up(m, 8) - cs + 7) >> 3;
-      for (int u = warp; u < nrb * 3; u += nw) {
-        const int rbk = u / 3, f = u % 3;
-        const int i = cs + 8 * rbk + g;
-        const int col = c1 + 8 * f + 2 * t;
-        if (c1 + 8 * f >= c2) continue;
-        double c0v = (col < c2) ? A[i + col * lda] : 0.0;
-        double c1v = (col + 1 < c2) ? A[i + (col + 1) * lda] : 0.0;
-#pragma unroll
-        for (int kk = 0; kk < kSub; kk += 4) {
-          const int q = kk + t;
-          const double av = (q < nsub && i >= cs + q) ? (i == cs + q ? 1.0 : A[i + (cs + q) * lda]) : 0.0;
-          const double bv = -wfin[q * 24 + 8 * f + g];
-          dmma8x8x4(c0v, c1v, av, bv);
-        }
-        if (col < c2) A[i + col * lda] = c0v;
-        if (col + 1 < c2) A[i + (col + 1) * lda] = c1v;
-      }
-    }
-    gsync<NTG>();
-    if (ltid<NTG>() == 0) HQR_STEP(43 + (jq >> 3) * 4);
-  }
-}
-
 // Whole-panel factorisation (no sub-panels).  NW warps; warp w owns panel
 // columns j0 + w + NW*u (u < CPW = 32/NW) in registers (rows j0 + lane + 32k).
 // Step j needs only pivot j: its owner publishes (column in A; tau / scale /
@@ -590,16 +378,6 @@ HBS_DEV void panel_factor_wide(double* A, int lda, int m, int j0, int nbp, doubl
   gsync<NTG>();
 }
 
-// Panel factorisation with 8-lane column groups (warps 0..7 of the CTA).
-// Lane group lg = lane / 8 of warp w owns panel column q = 4w + lg; lane
-// li = lane % 8 of the group holds rows j0 + li + 8k (k < MR8) in registers.
-// Every column-dot reduction is a 3-stage xor shuffle inside the group, and
-// the four groups of a warp reduce in the same shuffle instructions.  Step j
-// needs only pivot j (mbarrier hand-off from the warp owning it); a step is
-// bound by the FP64 and shuffle/shared pipes the active warps share, so warp
-// w stops after step 4w+3 (its columns are all reflectors by then) and only
-// the publishing warp runs the next pivot's norm.  The compact-WY dots
-// V^T V for form_t come from one tensor-core Gram product afterwards.
 template <int NTG>
 HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G);
 
@@ -796,152 +574,6 @@ HBS_DEV void panel_factor_r(double* A, int lda, int m, int j0, int nbp, double* 
   gsync<NTG>();
 }
 
-template <int MR8, int NTG>
-HBS_DEV void panel_factor_q(double* A, int lda, int m, int j0, int nbp, double* s_tau, double* s_scale,
-                            double* s_beta, uint64_t* bar, unsigned parity, double* G, double* s_an) {
-  // s_an[j] = alpha (pre-reflection diagonal), s_an[32 + j] = ||x||^2 of pivot j:
-  // the publisher stores only these; every warp forms the reflector itself,
-  // overlapped with its own loads and reductions (off the critical chain).
-  const int warp = (ltid<NTG>() >> 5), lane = ltid<NTG>() & 31;
-  if (warp < 8) {
-    const int lg = lane >> 3, li = lane & 7, gbase = lane & 24;
-    // contiguous columns per warp: warp w retires after step 4w+3 and leaves
-    // the pipes to the warps still updating
-    const int q = 4 * warp + lg, c = j0 + q, jlast = 4 * warp + 3;
-    const bool own = q < nbp;
-    const int kc = (m - j0 + 7) >> 3;
-    double x[MR8];
-#pragma unroll
-    for (int k = 0; k < MR8; ++k) x[k] = (own && k < kc) ? A[(j0 + li + 8 * k) + c * lda] : 0.0;
-    if (warp == 0) {  // first pivot j0 = column q 0 (warp 0, group 0): exact norm
-      double p = 0.0;
-#pragma unroll
-      for (int k = 0; k < MR8; ++k)
-        if (k < kc && li + 8 * k > 0) p = fma(x[k], x[k], p);
-      p += __shfl_xor_sync(0xffffffffu, p, 4);
-      p += __shfl_xor_sync(0xffffffffu, p, 2);
-      p += __shfl_xor_sync(0xffffffffu, p, 1);
-      const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
-      if (lane == 0) {
-        s_an[0] = alpha; s_an[32] = p;
-        mbar_arrive(&bar[0]);
-      }
-    }
-#pragma unroll
-    for (int kb = 0; kb < 4; ++kb) {          // row slot of the pivot: kb = j / 8 (compile time)
-      for (int jl = 0; jl < 8; ++jl) {
-        const int j = 8 * kb + jl, jj = j0 + j;
-        if (j >= nbp || j > jlast) break;
-        const bool tr = (j == 6) && own && (q == 7) && li == 0;
-        // warp-uniform: this warp owns pivot j+1 (group (j+1)%4 of warp (j+1)/4).
-        // Only it runs the norm / publish work and its shuffles: the SM's
-        // shuffle and shared-memory pipes, shared by the eight warps, bound a step.
-        const bool pubw = warp == ((j + 1) >> 2) && j + 1 < nbp;
-        mbar_wait(&bar[j], parity);
-        if (tr) STEP_MARK(0);
-        double pv[MR8];
-#pragma unroll
-        for (int k = 0; k < MR8; ++k) {
-          const int row = j0 + li + 8 * k;
-          pv[k] = (k < kc && row > jj) ? A[row + jj * lda] : 0.0;
-        }
-        const Reflector hj = make_reflector(s_an[j], s_an[32 + j]);
-        const double tau = hj.tau, scale = hj.scale;
-        if (tr) STEP_MARK(1);
-        if (c == jj && li == 0) { s_tau[jj] = hj.tau; s_scale[jj] = hj.scale; s_beta[jj] = hj.beta; }
-        if (tr) STEP_MARK(2);
-        const bool pub = own && (q == j + 1);
-        // my value in row jj (slot kb, lane jl of my group)
-        const double r = __shfl_sync(0xffffffffu, x[kb], gbase | jl);
-        double dd[8] = {};
-#pragma unroll
-        for (int k = 0; k < MR8; ++k) dd[k & 7] = fma(pv[k], x[k], dd[k & 7]);
-        if (tr) STEP_MARK(3);
-        double d = ((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]));
-        // publisher warp: ||x||^2 and ||pv||^2 over rows > jj+1 (pre-update x),
-        // and the row-(jj+1) values of x and pv
-        double sxx = 0.0, spp = 0.0, xn_old = 0.0, pn = 0.0;
-        if (pubw) {
-          double sx[4] = {}, sp[4] = {};
-#pragma unroll
-          for (int k = 0; k < MR8; ++k)
-            if (li + 8 * k > j + 1) { sx[k & 3] = fma(x[k], x[k], sx[k & 3]); sp[k & 3] = fma(pv[k], pv[k], sp[k & 3]); }
-          sxx = (sx[0] + sx[1]) + (sx[2] + sx[3]);
-          spp = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-          const int nl = (jl == 7) ? gbase : (gbase | (jl + 1));
-          xn_old = __shfl_sync(0xffffffffu, (jl == 7) ? x[kb < 3 ? kb + 1 : kb] : x[kb], nl);
-          pn = __shfl_sync(0xffffffffu, (jl == 7) ? pv[kb < 3 ? kb + 1 : kb] : pv[kb], nl);
-        }
-        d += __shfl_xor_sync(0xffffffffu, d, 4);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        if (tr) STEP_MARK(4);
-        const double f = tau * (r + scale * d), gs = f * scale;
-        if (own && c > jj) {
-#pragma unroll
-          for (int k = 0; k < MR8; ++k) x[k] = fma(-gs, pv[k], x[k]);
-          if (li == jl) x[kb] -= f;
-        }
-        if (tr) STEP_MARK(5);
-        if (pubw) {
-          sxx += __shfl_xor_sync(0xffffffffu, sxx, 4);
-          spp += __shfl_xor_sync(0xffffffffu, spp, 4);
-          sxx += __shfl_xor_sync(0xffffffffu, sxx, 2);
-          spp += __shfl_xor_sync(0xffffffffu, spp, 2);
-          sxx += __shfl_xor_sync(0xffffffffu, sxx, 1);
-          spp += __shfl_xor_sync(0xffffffffu, spp, 1);
-          // next pivot: ||x'||^2 over rows > jj+1 = sxx - 2 gs sxp + gs^2 spp,
-          // recomputed exactly on cancellation; alpha = updated row jj+1
-          double nrm = fma(gs * gs, spp, fma(-2.0 * gs, d - pn * xn_old, sxx));
-          const double alpha = fma(-gs, pn, xn_old);
-          if (tr) STEP_MARK(6);
-          const bool need = pub && (!(nrm > 0.5 * sxx) || sxx == 0.0);
-          if (__any_sync(0xffffffffu, need)) {
-            double pp = 0.0;
-#pragma unroll
-            for (int k = 0; k < MR8; ++k)
-              if (k < kc && li + 8 * k > j + 1) pp = fma(x[k], x[k], pp);
-            pp += __shfl_xor_sync(0xffffffffu, pp, 4);
-            pp += __shfl_xor_sync(0xffffffffu, pp, 2);
-            pp += __shfl_xor_sync(0xffffffffu, pp, 1);
-            if (need) nrm = pp;
-          }
-          if (tr) STEP_MARK(7);
-          if (pub) {
-#pragma unroll
-            for (int k = 0; k < MR8; ++k)
-              if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
-          }
-          __syncwarp();
-          if (pub && li == 0) {
-            s_an[j + 1] = alpha; s_an[32 + j + 1] = nrm;
-            if (tr) STEP_MARK(8);
-            mbar_arrive(&bar[j + 1]);
-            if (tr) STEP_MARK(9);
-          }
-        }
-      }
-    }
-    if (own) {
-#pragma unroll
-      for (int k = 0; k < MR8; ++k)
-        if (k < kc) A[(j0 + li + 8 * k) + c * lda] = x[k];
-    }
-  }
-  gsync<NTG>();
-  for (int qq = 0; qq < nbp; ++qq) {   // finalise: v tails = x * scale, diagonal = beta
-    const int cc = j0 + qq;
-    const double sc = s_scale[cc];
-    for (int i = cc + ltid<NTG>(); i < m; i += gthreads<NTG>()) {
-      if (i > cc) A[i + cc * lda] *= sc;
-      else A[i + cc * lda] = s_beta[cc];
-    }
-  }
-  gsync<NTG>();
-  panel_gram<NTG>(A, lda, m, j0, nbp, G);   // compact-WY dots V^T V for form_t
-  gsync<NTG>();
-}
-
 // G = V_p^T V_p (32 x 32) on the tensor cores; warp w < 16 computes one 8x8 block.
 template <int NTG>
 HBS_DEV void panel_gram(const double* A, int lda, int m, int j0, int nbp, double* G) {
@@ -1097,183 +729,5 @@ HBS_DEV void tri_inverse32(const double* A, int lda, int j0, int nbp, double* ou
 
 }  // namespace
 
-// Panel factorisation by CholeskyQR + Householder reconstruction (Ballard et
-// al.), for the fused kernel's panel group (NTG threads, named barrier 1).
-// The panel block P = A(j0:m, j0:j0+32) (rows below the finished R):
-//   Gp = P^T P = R^T R (tensor cores; Cholesky, row-owned, one warp),
-//   Q1 = P R^{-1} (tensor cores, in place),
-//   Q1(0:32, :) - S = L U with s_j = -sign of the current pivot (one warp),
-//   L2 = Q1(32:, :) U^{-1} (tensor cores, in place),
-//   T = -U S L^{-T}, R_hh = S R.
-// In exact arithmetic these are the reflectors (and T, R) the column-by-column
-// Householder chain (dlarfg signs) produces -- Householder QR is unique for a
-// given sign rule -- so the panel leaves A / T exactly as panel_factor_r +
-// form_t would, without a 32-step reduction chain.  Returns false (group-
-// uniform) for panels the chain must factor: partial panels, a Cholesky
-// breakdown, or min R_ii < 1e-2 max R_ii (the Gram squares the panel's
-// condition number; the chain also carries the reference's sigma screen).
-template <int NTG>
-static __device__ __noinline__ bool panel_factor_gram(double* A, int lda, int m, int j0, int nbp, double* G, double* T,
-                                               double* scr, int* s_flag) {
-  if (nbp != kP) return false;
-  const int warp = ltid<NTG>() >> 5, lane = ltid<NTG>() & 31, nw = gthreads<NTG>() >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int mp = round_up(m, 8);
-  double* sg = scr;   // signs s_j
-  // 1. Gp = P^T P (32 x 32, row-major in G): 16 tiles of 8 x 8
-  for (int tile = warp; tile < 16; tile += nw) {
-    const int fi = tile >> 2, fj = tile & 3;
-    const double* ci = A + (j0 + 8 * fi + g) * lda + t;
-    const double* cj = A + (j0 + 8 * fj + g) * lda + t;
-    double c[4][2] = {};
-    for (int k = j0; k < mp; k += 16) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (k + 4 * u < mp) dmma8x8x4(c[u][0], c[u][1], ci[k + 4 * u], cj[k + 4 * u]);
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      G[(8 * fi + g) * kLdT + 8 * fj + 2 * t + e] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
-  }
-  gsync<NTG>();
-  // 2. Cholesky (row i in lane i), R into G's upper triangle; R^{-1} into T
-  if (warp == 0) {
-    double c[kP];
-#pragma unroll
-    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? G[lane * kLdT + k] : 0.0;
-    const double gmax = warp_max(G[lane * kLdT + lane]);
-    bool ok = gmax > 0.0 && gmax < 1e300;
-#pragma unroll
-    for (int j = 0; j < kP; ++j) {
-      const double d = __shfl_sync(0xffffffffu, c[j], j);
-      ok = ok && (d > 1e-4 * gmax);                  // R_jj >= 1e-2 max R_ii (approximately)
-      const double rs = rsqrt_nr(d);
-      if (lane == j) {
-#pragma unroll
-        for (int k = 0; k < kP; ++k)
-          if (k >= j) c[k] *= rs;
-      }
-      double rji = 0.0;
-#pragma unroll
-      for (int k = j + 1; k < kP; ++k) {
-        const double rk = __shfl_sync(0xffffffffu, c[k], j);
-        if (k == lane) rji = rk;
-        if (lane > j && k >= lane) c[k] = fma(-rji, rk, c[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kP; ++k)
-      if (k >= lane) G[lane * kLdT + k] = c[k];
-    __syncwarp();
-    // row lane of R^{-1}: x R = e_lane
-#pragma unroll
-    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < kP; ++k) {
-      c[k] *= rcp_nr(G[k * kLdT + k]);
-#pragma unroll
-      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], G[k * kLdT + l], c[l]);
-    }
-#pragma unroll
-    for (int k = 0; k < kP; ++k) T[lane * kLdT + k] = c[k];
-    if (lane == 0) *s_flag = __all_sync(0xffffffffu, ok) ? 1 : 0;
-    else __all_sync(0xffffffffu, ok);
-  }
-  gsync<NTG>();
-  if (!*s_flag) return false;
-  // 3. Q1 = P R^{-1} in place, 8-row blocks per warp
-  for (int r0 = j0 + 8 * warp; r0 < mp; r0 += 8 * nw) {
-    double a[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
-    double acc[4][2] = {};
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
-    __syncwarp();
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
-  }
-  gsync<NTG>();
-  // 4. sign-chosen LU of the top 32 x 32 block (row lane in lane); U^{-1}
-  //    into T (R^{-1} is dead); R_hh = S R into A's upper triangle (U is dead
-  //    once U^{-1} and the T rows are formed); T = -U S L^{-T} rows into G
-  if (warp == 0) {
-    double c[kP];
-#pragma unroll
-    for (int k = 0; k < kP; ++k) c[k] = A[(j0 + lane) + (j0 + k) * lda];
-#pragma unroll
-    for (int j = 0; j < kP; ++j) {
-      double dinv = 0.0;
-      if (lane == j) {
-        const double sj = c[j] >= 0.0 ? -1.0 : 1.0;
-        c[j] -= sj;
-        sg[j] = sj;
-        dinv = rcp_nr(c[j]);
-      }
-      dinv = __shfl_sync(0xffffffffu, dinv, j);
-      const double l = c[j] * dinv;
-      if (lane > j) c[j] = l;
-#pragma unroll
-      for (int k = j + 1; k < kP; ++k) {
-        const double uk = __shfl_sync(0xffffffffu, c[k], j);
-        if (lane > j) c[k] = fma(-l, uk, c[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kP; ++k) A[(j0 + lane) + (j0 + k) * lda] = c[k];
-    __syncwarp();
-    // column lane of U^{-1}: U z = e_lane, back substitution (c reused)
-#pragma unroll
-    for (int k = 0; k < kP; ++k) c[k] = (k == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = kP - 1; k >= 0; --k) {
-      c[k] *= rcp_nr(A[(j0 + k) + (j0 + k) * lda]);
-#pragma unroll
-      for (int q = 0; q < k; ++q) c[q] = fma(-A[(j0 + q) + (j0 + k) * lda], c[k], c[q]);
-    }
-#pragma unroll
-    for (int k = 0; k < kP; ++k) T[k * kLdT + lane] = c[k];
-    // T row lane: -(U S) then forward substitution with L (unit lower)
-#pragma unroll
-    for (int k = 0; k < kP; ++k) c[k] = (k >= lane) ? -A[(j0 + lane) + (j0 + k) * lda] * sg[k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kP; ++k)
-#pragma unroll
-      for (int l = k + 1; l < kP; ++l) c[l] = fma(-c[k], A[(j0 + l) + (j0 + k) * lda], c[l]);
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kP; ++k)
-      if (k >= lane) A[(j0 + lane) + (j0 + k) * lda] = sg[lane] * G[lane * kLdT + k];
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kP; ++k) G[lane * kLdT + k] = c[k];
-  }
-  gsync<NTG>();
-  // 5. L2 = Q1(32:, :) U^{-1} in place
-  for (int r0 = j0 + kP + 8 * warp; r0 < mp; r0 += 8 * nw) {
-    double a[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) a[kk] = A[(r0 + g) + (j0 + 4 * kk + t) * lda];
-    double acc[4][2] = {};
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-      for (int f = 0; f < 4; ++f) dmma8x8x4(acc[f][0], acc[f][1], a[kk], T[(4 * kk + t) * kLdT + 8 * f + g]);
-    __syncwarp();
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * f + 2 * t + e) * lda] = acc[f][e];
-  }
-  gsync<NTG>();
-  // 6. T from G
-  for (int e = ltid<NTG>(); e < kP * kP; e += gthreads<NTG>()) T[(e / kP) * kLdT + e % kP] = G[(e / kP) * kLdT + e % kP];
-  gsync<NTG>();
-  return true;
-}
 
 }  // namespace hbs
